@@ -1,0 +1,158 @@
+/*
+ * flexq.h -- C ABI of the B200 (sm_100a) W6A6/W6A8 quantized-linear library
+ * (libflexq_sm100a.so).  Plain pointers, sizes and a cudaStream_t; no torch
+ * types.  All pointers are DEVICE pointers unless stated; nothing here
+ * allocates memory on the hot path (workspaces are caller-owned).
+ *
+ * The reference (FlexQ restatement, package `bitserial`) is pure Python; its
+ * FFI for this path would bind one C entry per public Python function.  Each
+ * entry below names the reference interface it replaces
+ * (paths under /root/reference/pkg/src/bitserial/).  INTEGRATION.md shows the
+ * ctypes stub a maintainer would add.
+ *
+ * Errors: every entry returns an int status (0 = ok, negative = error) and
+ * records a message retrievable with flexq_last_error() (thread-local).  The
+ * codes map 1:1 to the reference's exception classes (errors.py:8-28).
+ * Data-dependent errors (non-finite input, a scale that rounds to zero) are
+ * detected on the device and OR-ed into a caller-provided int32 flag word.
+ */
+#ifndef FLEXQ_H_
+#define FLEXQ_H_
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:4-28) ---------------------------------------- */
+#define FLEXQ_OK 0
+#define FLEXQ_ERR_INVALID_INPUT (-1) /* InvalidInputError  (errors.py:8)  */
+#define FLEXQ_ERR_SHAPE (-2)         /* ShapeError         (errors.py:12) */
+#define FLEXQ_ERR_CONFIG (-3)        /* ConfigError        (errors.py:16) */
+#define FLEXQ_ERR_FORMAT (-4)        /* FormatError        (errors.py:24) */
+#define FLEXQ_ERR_CUDA (-5)          /* CUDA runtime / launch failure      */
+
+/* device flag bits written by the quantizers */
+#define FLEXQ_FLAG_NONFINITE 1u      /* quantize.py:135-136 "input contains non-finite values" */
+#define FLEXQ_FLAG_NONPOS_SCALE 2u   /* quantize.py:71-72   "all scales must be strictly positive" */
+
+/* float input dtypes */
+#define FLEXQ_DT_F16 0
+#define FLEXQ_DT_BF16 1
+#define FLEXQ_DT_F32 2
+#define FLEXQ_DT_F64 3
+
+/* output dtypes for the fast epilogue */
+#define FLEXQ_OUT_F16 0
+#define FLEXQ_OUT_F32 1
+
+const char* flexq_last_error(void);
+int flexq_version(void);                  /* MAJOR*10000 + MINOR*100 + PATCH */
+int flexq_device_check(void);             /* 0 if an sm_100 device is current, else FLEXQ_ERR_CUDA */
+
+/* ---- quantizer ------------------------------------------------------------
+ * Replaces quantize(data, bits, group_size, fp16_scales)  (quantize.py:118-148).
+ * x: [rows, cols] row-major, dtype `dtype`.  codes: int8 [rows, cols] or NULL.
+ * scales: float64 [rows, G] or NULL, G = ceil(cols / group_size).
+ * Bit-exact with the reference: float64 divide, half-away rounding, fp16
+ * scale rounding directly from float64.  Optional fused outputs for the i8
+ * GEMM path (NULL to skip): act_frag (T6 activation fragment layout, see
+ * DESIGN.md sec. 3), act_scale_f32 [G, m_pad], act_corr [G, m_pad] (= 32 * sum of
+ * codes per group, the offset-binary weight correction).  `m_pad` is the token
+ * stride of those arrays (multiple of 8 >= rows). */
+int flexq_quantize(const void* x, int dtype, int64_t rows, int64_t cols, int bits,
+                   int64_t group_size, int fp16_scales, int8_t* codes, double* scales,
+                   uint32_t* act_frag, float* act_scale_f32, int32_t* act_corr, int64_t m_pad,
+                   uint32_t* flag, cudaStream_t stream);
+
+/* ---- bit-plane packer (FLXQ-P, byte-identical with the reference) ---------
+ * Replaces pack(decompose(q), PackConfig(chunk_m, word_bits))  (bitplane.py:55-84,
+ * packing.py:132-147, docs/format.md:47-84).  codes int8 [rows, cols] ->
+ * words [KC, RC, bits, chunk_m, 16 bytes] (little-endian, LSB-first). */
+int64_t flexq_planes_bytes(int64_t rows, int64_t cols, int bits, int chunk_m);
+int flexq_pack_planes(const int8_t* codes, int64_t rows, int64_t cols, int bits, int chunk_m,
+                      uint8_t* words, cudaStream_t stream);
+/* Replaces recompose(unpack(p, cfg))  (packing.py:150-165, bitplane.py:87-89). */
+int flexq_unpack_planes(const uint8_t* words, int64_t rows, int64_t cols, int bits, int chunk_m,
+                        int8_t* codes, cudaStream_t stream);
+
+/* ---- T6 weight layout for the unpack-to-INT8 tensor-core path -------------
+ * The offline packer of the production path (weight_pack_config analogue,
+ * packing.py:74-76): 6-bit codes in offset binary (u = code + 32) split into
+ * the low-nibble planes {0..3} and the high planes {4,5}, laid out so every
+ * lane's 16-byte loads are its mma A-fragments.  Requires |code| <= 31 (bits<=6).
+ * weights: int8 [n, k];  scales float64 [n, G].  t6: u32 [RT, KB, 3, 32, 4];
+ * wscale: [RT, G, 8, 2] in fp16 (scale_f16=1, exact only in fp16-scale mode)
+ * or fp32. */
+int64_t flexq_t6_bytes(int64_t n, int64_t k, int64_t group_size);
+int flexq_pack_t6(const int8_t* codes, const double* scales, int64_t n, int64_t k,
+                  int64_t group_size, int scale_f16, uint32_t* t6, void* wscale,
+                  cudaStream_t stream);
+int64_t flexq_act_frag_bytes(int64_t m_pad, int64_t k, int64_t group_size);
+/* Already-quantized activations (a QuantTensor: int8 codes [m, k] + float64
+ * scales [m, G]) -> the T6 activation operand, for int_matmul_reference-style
+ * calls (engine.py:337-365) that skip the float quantizer. */
+int flexq_pack_act_t6(const int8_t* codes, const double* scales, int64_t m, int64_t m_pad,
+                      int64_t k, int64_t group_size, uint32_t* act_frag, float* act_scale_f32,
+                      int32_t* act_corr, cudaStream_t stream);
+/* Replaces bmma_chunk (engine.py:89-95): *out = sum popcount(a[i] & b[i]) over
+ * nbytes bytes (device int64 result). */
+int flexq_popcount_and(const uint8_t* a, const uint8_t* b, int64_t nbytes, int64_t* out,
+                       cudaStream_t stream);
+
+/* ---- GEMM cores ------------------------------------------------------------
+ * Both produce, per (token m, row n, group g), the exact integer partial
+ * P[g,m,n] = sum_{k in g} x[m,k]*w[n,k] and then either
+ *   trace:  P written as int32 [G, m, n]   (engine.py:211-216 trace_slot;
+ *           caller zeroes it: partial groups are combined with integer atomics)
+ *   fast:   y[m,n] = sum_g (xs*ws) * P in fp32, stored fp16/fp32 [m, n].
+ * `partials` / `y` may be NULL to skip either.  workspace: see
+ * flexq_gemm_workspace_bytes (fp32 split-K partials + per-tile counters; the
+ * counters must be zero before the first call and are left zeroed). */
+int64_t flexq_gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t group_size,
+                                   int ksplit /* 0 = auto */);
+
+/* Production path: unpack-to-INT8 + tensor cores over T6 weights.
+ * Replaces int_matmul_reference / group_matmul_fused numerics (engine.py:290-365).
+ * act_* are the fused outputs of flexq_quantize (same m_pad). */
+int flexq_gemm_t6(const uint32_t* t6, const void* wscale, int scale_f16,
+                  const uint32_t* act_frag, const float* act_scale, const int32_t* act_corr,
+                  int64_t m, int64_t m_pad, int64_t n, int64_t k, int64_t group_size,
+                  int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
+                  cudaStream_t stream);
+
+/* BTC-equivalent bit-serial path: AND + popcount over FLXQ-P planes.
+ * Replaces group_matmul_fused(wp, xp, ...)  (engine.py:290-334): wwords /
+ * xwords from flexq_pack_planes with their chunk_m (reference defaults: 8 for
+ * weights, min(m, 8) for activations, packing.py:69-76); scales fp32
+ * row-major [n, G] / [m, G] (fast epilogue only). */
+int flexq_gemm_bitserial(const uint8_t* wwords, const uint8_t* xwords, const float* wscale,
+                         const float* xscale, int64_t m, int64_t n, int64_t k, int wbits,
+                         int xbits, int64_t group_size, int w_chunk_m, int x_chunk_m,
+                         int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
+                         cudaStream_t stream);
+
+/* Exact float64 epilogue over traced partials: y[m,n] = sum_g (xs*ws)*P in
+ * ascending g with separate IEEE multiply/add -- bit-identical with the
+ * reference's _scale_accumulate (engine.py:211-216).  y16 (fp16, correctly
+ * rounded from the float64 result) may be NULL. */
+int flexq_group_epilogue_f64(const int32_t* partials, const double* wscale,
+                             const double* xscale, int64_t m, int64_t n, int64_t groups,
+                             double* y, uint16_t* y16, cudaStream_t stream);
+
+/* ---- one-call online linear (quantized_linear with pre-packed weights) ----
+ * Replaces the online half of quantized_linear (engine.py:487-513):
+ * quantize activations (fp16 [m, k]) -> T6 GEMM -> fp16 y [m, n].
+ * act_buf must hold flexq_act_buf_bytes(); workspace flexq_gemm_workspace_bytes(). */
+int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size);
+int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
+                         const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
+                         uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
+                         cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXQ_H_ */

@@ -1,0 +1,217 @@
+// extern "C" boundary of libflexq_sm100a.so (declared in include/flexq.h).
+// Argument validation here mirrors the reference's raising sites so the
+// Python wrapper can map status codes to the same exception classes.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace flexq {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  set_error("%s: CUDA error %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+  return FLEXQ_ERR_CUDA;
+}
+
+int quantize_launch(const void*, int, int64_t, int64_t, int, int64_t, int, int8_t*, double*,
+                    uint32_t*, float*, int32_t*, int64_t, uint32_t*, cudaStream_t);
+int pack_planes_launch(const int8_t*, int64_t, int64_t, int, int, uint8_t*, cudaStream_t);
+int unpack_planes_launch(const uint8_t*, int64_t, int64_t, int, int, int8_t*, cudaStream_t);
+int pack_t6_launch(const int8_t*, const double*, int64_t, int64_t, int64_t, int, uint32_t*, void*,
+                   cudaStream_t);
+int64_t gemm_t6_workspace(int64_t, int64_t, int64_t, int64_t, int);
+int gemm_t6_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
+                   const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
+                   int, void*, int, cudaStream_t);
+int64_t gemm_bitserial_workspace(int64_t, int64_t, int64_t, int);
+int gemm_bitserial_launch(const uint8_t*, const uint8_t*, const float*, const float*, int64_t,
+                          int64_t, int64_t, int, int, int64_t, int, int, int32_t*, void*, int,
+                          void*, int, cudaStream_t);
+int codes_to_frag_launch(const int8_t*, const double*, int64_t, int64_t, int64_t, int64_t,
+                         uint32_t*, float*, int32_t*, cudaStream_t);
+int popcount_and_launch(const uint8_t*, const uint8_t*, int64_t, int64_t*, cudaStream_t);
+int group_epilogue_launch(const int32_t*, const double*, const double*, int64_t, int64_t, int64_t,
+                          double*, uint16_t*, cudaStream_t);
+
+static int check_chunk_m(int cm) {
+  if (cm < 1 || cm > 8) {
+    set_error("chunk_m (%d) must be in 1..8", cm);
+    return FLEXQ_ERR_CONFIG;
+  }
+  return FLEXQ_OK;
+}
+
+}  // namespace flexq
+
+using namespace flexq;
+
+extern "C" {
+
+const char* flexq_last_error(void) { return g_err; }
+
+int flexq_version(void) { return 100; /* 0.1.0 */ }
+
+int flexq_device_check(void) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "flexq_device_check");
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) {
+    set_error("libflexq_sm100a needs an sm_100 (B200) device, found sm_%d%d", major, minor);
+    return FLEXQ_ERR_CUDA;
+  }
+  return FLEXQ_OK;
+}
+
+int flexq_quantize(const void* x, int dtype, int64_t rows, int64_t cols, int bits,
+                   int64_t group_size, int fp16_scales, int8_t* codes, double* scales,
+                   uint32_t* act_frag, float* act_scale_f32, int32_t* act_corr, int64_t m_pad,
+                   uint32_t* flag, cudaStream_t stream) {
+  return quantize_launch(x, dtype, rows, cols, bits, group_size, fp16_scales, codes, scales,
+                         act_frag, act_scale_f32, act_corr, m_pad, flag, stream);
+}
+
+int64_t flexq_planes_bytes(int64_t rows, int64_t cols, int bits, int chunk_m) {
+  if (chunk_m < 1) return 0;
+  return cdiv(cols, kChunkK) * cdiv(rows, chunk_m) * bits * chunk_m * 16;
+}
+
+int flexq_pack_planes(const int8_t* codes, int64_t rows, int64_t cols, int bits, int chunk_m,
+                      uint8_t* words, cudaStream_t stream) {
+  int rc = check_chunk_m(chunk_m);
+  if (rc) return rc;
+  if (bits < 1 || bits > 8) {
+    set_error("bits must be in 1..8, got %d", bits);
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  if (rows < 1 || cols < 1) {
+    set_error("pack_planes: empty tensor (%lld, %lld)", (long long)rows, (long long)cols);
+    return FLEXQ_ERR_SHAPE;
+  }
+  return pack_planes_launch(codes, rows, cols, bits, chunk_m, words, stream);
+}
+
+int flexq_unpack_planes(const uint8_t* words, int64_t rows, int64_t cols, int bits, int chunk_m,
+                        int8_t* codes, cudaStream_t stream) {
+  int rc = check_chunk_m(chunk_m);
+  if (rc) return rc;
+  if (bits < 1 || bits > 8 || rows < 1 || cols < 1) {
+    set_error("unpack_planes: bad geometry rows=%lld cols=%lld bits=%d", (long long)rows,
+              (long long)cols, bits);
+    return FLEXQ_ERR_FORMAT;
+  }
+  return unpack_planes_launch(words, rows, cols, bits, chunk_m, codes, stream);
+}
+
+int64_t flexq_t6_bytes(int64_t n, int64_t k, int64_t group_size) {
+  T6Geom G(n, k, group_size);
+  return G.rt * G.kb * 3 * 32 * 16;
+}
+
+int64_t flexq_act_frag_bytes(int64_t m_pad, int64_t k, int64_t group_size) {
+  T6Geom G(1, k, group_size);
+  return cdiv(m_pad, kTokTile) * G.kb * 32 * 32;
+}
+
+int flexq_pack_t6(const int8_t* codes, const double* scales, int64_t n, int64_t k,
+                  int64_t group_size, int scale_f16, uint32_t* t6, void* wscale,
+                  cudaStream_t stream) {
+  if (n < 1 || k < 1 || group_size < 1) {
+    set_error("pack_t6: bad geometry n=%lld k=%lld group=%lld", (long long)n, (long long)k,
+              (long long)group_size);
+    return FLEXQ_ERR_SHAPE;
+  }
+  if (wscale && !scales) {
+    set_error("pack_t6: scales required to pack wscale");
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  return pack_t6_launch(codes, scales, n, k, group_size, scale_f16, t6, wscale, stream);
+}
+
+int flexq_pack_act_t6(const int8_t* codes, const double* scales, int64_t m, int64_t m_pad,
+                      int64_t k, int64_t group_size, uint32_t* act_frag, float* act_scale_f32,
+                      int32_t* act_corr, cudaStream_t stream) {
+  return codes_to_frag_launch(codes, scales, m, m_pad, k, group_size, act_frag, act_scale_f32,
+                              act_corr, stream);
+}
+
+int flexq_popcount_and(const uint8_t* a, const uint8_t* b, int64_t nbytes, int64_t* out,
+                       cudaStream_t stream) {
+  return popcount_and_launch(a, b, nbytes, out, stream);
+}
+
+int64_t flexq_gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t group_size,
+                                   int ksplit) {
+  int64_t a = gemm_t6_workspace(m, n, k, group_size, ksplit);
+  int64_t b = gemm_bitserial_workspace(m, n, k, ksplit);
+  return a > b ? a : b;
+}
+
+int flexq_gemm_t6(const uint32_t* t6, const void* wscale, int scale_f16,
+                  const uint32_t* act_frag, const float* act_scale, const int32_t* act_corr,
+                  int64_t m, int64_t m_pad, int64_t n, int64_t k, int64_t group_size,
+                  int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
+                  cudaStream_t stream) {
+  return gemm_t6_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
+                        group_size, partials, y, out_dtype, workspace, ksplit, stream);
+}
+
+int flexq_gemm_bitserial(const uint8_t* wwords, const uint8_t* xwords, const float* wscale,
+                         const float* xscale, int64_t m, int64_t n, int64_t k, int wbits,
+                         int xbits, int64_t group_size, int w_chunk_m, int x_chunk_m,
+                         int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
+                         cudaStream_t stream) {
+  return gemm_bitserial_launch(wwords, xwords, wscale, xscale, m, n, k, wbits, xbits, group_size,
+                               w_chunk_m, x_chunk_m, partials, y, out_dtype, workspace, ksplit,
+                               stream);
+}
+
+int flexq_group_epilogue_f64(const int32_t* partials, const double* wscale,
+                             const double* xscale, int64_t m, int64_t n, int64_t groups,
+                             double* y, uint16_t* y16, cudaStream_t stream) {
+  return group_epilogue_launch(partials, wscale, xscale, m, n, groups, y, y16, stream);
+}
+
+int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size) {
+  const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
+  T6Geom G(1, k, group_size);
+  const int64_t frag = cdiv(flexq_act_frag_bytes(m_pad, k, group_size), 256) * 256;
+  const int64_t vec = cdiv(G.ng * m_pad * 4, 256) * 256;
+  return frag + 2 * vec;
+}
+
+int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
+                         const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
+                         uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
+                         cudaStream_t stream) {
+  if (!act_buf || !flag || !y) {
+    set_error("linear_forward: act_buf, flag and y are required");
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
+  T6Geom G(1, k, group_size);
+  char* base = reinterpret_cast<char*>(act_buf);
+  const int64_t frag = cdiv(flexq_act_frag_bytes(m_pad, k, group_size), 256) * 256;
+  const int64_t vec = cdiv(G.ng * m_pad * 4, 256) * 256;
+  uint32_t* act_frag = reinterpret_cast<uint32_t*>(base);
+  float* xs = reinterpret_cast<float*>(base + frag);
+  int32_t* corr = reinterpret_cast<int32_t*>(base + frag + vec);
+  int rc = quantize_launch(x, FLEXQ_DT_F16, m, k, xbits, group_size, 1, nullptr, nullptr,
+                           act_frag, xs, corr, m_pad, flag, stream);
+  if (rc) return rc;
+  return gemm_t6_launch(t6, wscale, scale_f16, act_frag, xs, corr, m, m_pad, n, k, group_size,
+                        nullptr, y, FLEXQ_OUT_F16, workspace, 0, stream);
+}
+
+}  // extern "C"

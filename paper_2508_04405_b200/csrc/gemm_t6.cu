@@ -1,0 +1,371 @@
+// Production GEMV/GEMM core: unpack-to-INT8 on the tensor cores.
+//
+// Replaces the numerics of group_matmul_fused / int_matmul_reference
+// (engine.py:251-365): per (token m, row n, scale group g) the exact integer
+//   P[g,m,n] = sum_{k in g} x[m,k] * w[n,k]
+// followed by the fused dequant y[m,n] = sum_g (xs[m,g]*ws[n,g]) * P
+// (engine.py:211-216).
+//
+// Why not the bit-serial BMMA of the paper on B200: sm_100a has no binary
+// tensor core (mma .b1 lowers to IMMA + MOVM emulation) and POPC issues at
+// 16/clk/SM (measured, tools/probe/rates.cu), so AND+popcount caps a W6A8 GEMV
+// at ~35% of HBM roofline.  Unpacking the 6-bit codes costs ~0.75 ALU op per
+// weight and feeds mma.sync.m16n8k32 (IMMA, measured 1.15 POPS), which keeps
+// the layer HBM-bound for the decode batches this kernel serves.
+//
+// Operands:
+//   T6 weights   u32 [RT][KB][3][32 lanes][4]: per lane per k-step three words
+//                L0/L1 (low nibbles) and H (2-bit highs) of 16 offset-binary
+//                codes u = w + 32 -> the four A registers of one mma.
+//   act fragments u32 [MT][KB][32 lanes][8]: per lane per k-step the two B
+//                registers (int8 codes).
+//   Because A holds u = w + 32, the group partial is sum u*x - 32*sum x; the
+//   second term (act_corr) seeds the accumulator of the group's first k-step.
+//
+// Work split: CTA = (16-row tile, K range); its 4 warps take interleaved
+// k-blocks (128 k-slots, 3 x LDG.128 per lane).  A warp's fp32 partial sums
+// are reduced across warps in fixed order, then across K-split CTAs by the
+// last-arriving CTA in fixed order -> deterministic output.
+#include "common.cuh"
+
+namespace flexq {
+
+struct T6Params {
+  const uint4* __restrict__ t6;
+  const void* __restrict__ wscale;
+  const uint4* __restrict__ act;
+  const float* __restrict__ xs;
+  const int32_t* __restrict__ corr;
+  int64_t m, m_pad, n;          // m: valid tokens of this chunk; m_pad: stride of xs/corr
+  int64_t m_total, tok0;        // trace / output token indexing
+  int64_t ws_mstride;           // token stride of the split-K workspace
+  int64_t ng, spg, ks, kb, rt;
+  int32_t* partials;
+  void* y;
+  float* ws_part;
+  unsigned* counters;
+  int ksplit;
+};
+
+__device__ __forceinline__ void unpack_t6(uint32_t L0, uint32_t L1, uint32_t H, uint32_t a[4]) {
+  a[0] = (L0 & 0x0F0F0F0Fu) | ((H & 0x03030303u) << 4);
+  a[1] = ((L0 >> 4) & 0x0F0F0F0Fu) | ((H & 0x0C0C0C0Cu) << 2);
+  a[2] = (L1 & 0x0F0F0F0Fu) | (H & 0x30303030u);
+  a[3] = ((L1 >> 4) & 0x0F0F0F0Fu) | ((H >> 2) & 0x30303030u);
+}
+
+__device__ __forceinline__ void mma_u8s8(int c[4], const uint32_t a[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Weights are read exactly once: bypass L1 and mark the L2 lines evict-first
+// (the paper's evict_first hint) so the L2-resident
+// activation fragments and scales are not displaced.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t u4get(const uint4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+template <bool SF16>
+__device__ __forceinline__ float2 load_wscale(const void* ws, int64_t idx) {
+  if constexpr (SF16) {
+    __half2 h = reinterpret_cast<const __half2*>(ws)[idx];
+    return __half22float2(h);
+  } else {
+    return reinterpret_cast<const float2*>(ws)[idx];
+  }
+}
+
+template <int OUT>
+__device__ __forceinline__ void store_y(void* y, int64_t i, float v) {
+  if constexpr (OUT == FLEXQ_OUT_F16)
+    reinterpret_cast<__half*>(y)[i] = __float2half_rn(v);
+  else
+    reinterpret_cast<float*>(y)[i] = v;
+}
+
+constexpr int kT6Warps = 4;
+
+template <int MT, bool SF16, bool TRACE, bool FAST, int OUT>
+__global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, t = lane & 3;
+  const int64_t rt = blockIdx.x, split = blockIdx.y;
+  const int64_t kb0 = split * p.kb / p.ksplit, kb1 = (split + 1) * p.kb / p.ksplit;
+  const int64_t row0 = rt * kRowTile + gq, row1 = row0 + 8;
+
+  float acc[MT][4];
+  int P[MT][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+    for (int i = 0; i < 4; i++) { acc[mt][i] = 0.f; P[mt][i] = 0; }
+  int64_t cur = -1;
+
+  auto drain = [&](int64_t g) {
+    if constexpr (TRACE) {
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        const int64_t tok0 = mt * kTokTile + 2 * t;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int64_t tok = tok0 + (i & 1), row = (i & 2) ? row1 : row0;
+          if (tok < p.m && row < p.n)
+            atomicAdd(&p.partials[(g * p.m_total + p.tok0 + tok) * p.n + row], P[mt][i]);
+        }
+      }
+    }
+    if constexpr (FAST) {
+      const float2 sw = load_wscale<SF16>(p.wscale, (rt * p.ng + g) * 8 + gq);
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        const float2 sx = *reinterpret_cast<const float2*>(&p.xs[g * p.m_pad + mt * kTokTile + 2 * t]);
+        acc[mt][0] = fmaf(sw.x * sx.x, (float)P[mt][0], acc[mt][0]);
+        acc[mt][1] = fmaf(sw.x * sx.y, (float)P[mt][1], acc[mt][1]);
+        acc[mt][2] = fmaf(sw.y * sx.x, (float)P[mt][2], acc[mt][2]);
+        acc[mt][3] = fmaf(sw.y * sx.y, (float)P[mt][3], acc[mt][3]);
+      }
+    }
+  };
+
+  const uint4* wbase = p.t6 + rt * p.kb * 3 * 32 + lane;
+  const uint64_t pol = evict_first_policy();
+  int64_t kb = kb0 + warp;
+  uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0, w2 = w0;
+  if (kb < kb1) {
+    const uint4* q = wbase + kb * 96;
+    w0 = ld_stream(q, pol); w1 = ld_stream(q + 32, pol); w2 = ld_stream(q + 64, pol);
+  }
+  for (; kb < kb1; kb += kT6Warps) {
+    // prefetch the next k-block of this warp while the current one computes
+    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0, n2 = n0;
+    const int64_t kbn = kb + kT6Warps;
+    if (kbn < kb1) {
+      const uint4* q = wbase + kbn * 96;
+      n0 = ld_stream(q, pol); n1 = ld_stream(q + 32, pol); n2 = ld_stream(q + 64, pol);
+    }
+    uint4 b[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++) {
+      if (mt * kTokTile + gq < p.m) {
+        const uint4* q = p.act + ((mt * p.kb + kb) * 32 + lane) * 2;
+        b[mt][0] = __ldg(q); b[mt][1] = __ldg(q + 1);
+      } else {
+        b[mt][0] = make_uint4(0, 0, 0, 0); b[mt][1] = b[mt][0];
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 4; jj++) {
+      const int64_t ks = kb * 4 + jj;
+      if (ks >= p.ks) break;
+      const int64_t g = ks / p.spg;
+      if (g != cur) {
+        if (cur >= 0) drain(cur);
+        cur = g;
+        const bool first = (ks == g * p.spg);
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          int2 cr = make_int2(0, 0);
+          if (first) cr = *reinterpret_cast<const int2*>(&p.corr[g * p.m_pad + mt * kTokTile + 2 * t]);
+          P[mt][0] = -cr.x; P[mt][1] = -cr.y; P[mt][2] = -cr.x; P[mt][3] = -cr.y;
+        }
+      }
+      uint32_t a[4];
+      unpack_t6(u4get(w0, jj), u4get(w1, jj), u4get(w2, jj), a);
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        const uint4& bb = jj < 2 ? b[mt][0] : b[mt][1];
+        const uint32_t b0 = (jj & 1) ? bb.z : bb.x, b1 = (jj & 1) ? bb.w : bb.y;
+        mma_u8s8(P[mt], a, b0, b1);
+      }
+    }
+    w0 = n0; w1 = n1; w2 = n2;
+  }
+  if (cur >= 0) drain(cur);
+
+  if constexpr (FAST) {
+    __shared__ float red[kT6Warps][MT][4][32];
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int i = 0; i < 4; i++) red[warp][mt][i][lane] = acc[mt][i];
+    __syncthreads();
+    if (warp != 0) return;
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        float s = red[0][mt][i][lane];
+#pragma unroll
+        for (int w = 1; w < kT6Warps; w++) s += red[w][mt][i][lane];
+        acc[mt][i] = s;
+      }
+    const int64_t n_pad = p.rt * kRowTile;
+    if (p.ksplit > 1) {
+      // publish this CTA's partial; the last CTA of the row tile reduces in split order
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = (i & 2) ? row1 : row0;
+          p.ws_part[(split * p.ws_mstride + tok) * n_pad + row] = acc[mt][i];
+        }
+      __threadfence();
+      unsigned prev = 0;
+      if (lane == 0) prev = atomicAdd(&p.counters[rt], 1u);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev != (unsigned)p.ksplit - 1) return;
+      __threadfence();
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = (i & 2) ? row1 : row0;
+          float s = 0.f;
+          for (int sp = 0; sp < p.ksplit; sp++)
+            s += __ldcg(&p.ws_part[(sp * p.ws_mstride + tok) * n_pad + row]);
+          acc[mt][i] = s;
+        }
+      if (lane == 0) p.counters[rt] = 0u;
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = (i & 2) ? row1 : row0;
+        if (tok < p.m && row < p.n) store_y<OUT>(p.y, (p.tok0 + tok) * p.n + row, acc[mt][i]);
+      }
+  }
+}
+
+int auto_ksplit_t6(int64_t rt, int64_t kb) {
+  // aim for ~6 CTAs of 4 warps per SM (148 SMs) while keeping >= 2 k-blocks per warp
+  int64_t want = cdiv(148 * 6, rt);
+  int64_t cap = kb / (2 * kT6Warps);
+  if (cap < 1) cap = 1;
+  if (want > cap) want = cap;
+  if (want > 16) want = 16;
+  return (int)(want < 1 ? 1 : want);
+}
+
+template <int MT, bool SF16, bool TRACE, bool FAST, int OUT>
+static void launch_t6(const T6Params& p, cudaStream_t st) {
+  dim3 grid((unsigned)p.rt, (unsigned)p.ksplit);
+  gemm_t6_kernel<MT, SF16, TRACE, FAST, OUT><<<grid, kT6Warps * 32, 0, st>>>(p);
+}
+
+template <int MT>
+static void dispatch_t6(const T6Params& p, bool sf16, bool trace, bool fast, int out,
+                        cudaStream_t st) {
+#define FLEXQ_T6_CASE(SF, TR, FA, OU)                                   \
+  if (sf16 == SF && trace == TR && fast == FA && (!FA || out == OU)) { \
+    launch_t6<MT, SF, TR, FA, OU>(p, st);                              \
+    return;                                                            \
+  }
+  FLEXQ_T6_CASE(true, false, true, FLEXQ_OUT_F16)
+  FLEXQ_T6_CASE(true, false, true, FLEXQ_OUT_F32)
+  FLEXQ_T6_CASE(false, false, true, FLEXQ_OUT_F16)
+  FLEXQ_T6_CASE(false, false, true, FLEXQ_OUT_F32)
+  FLEXQ_T6_CASE(true, true, true, FLEXQ_OUT_F16)
+  FLEXQ_T6_CASE(true, true, true, FLEXQ_OUT_F32)
+  FLEXQ_T6_CASE(false, true, true, FLEXQ_OUT_F16)
+  FLEXQ_T6_CASE(false, true, true, FLEXQ_OUT_F32)
+  FLEXQ_T6_CASE(true, true, false, 0)
+  FLEXQ_T6_CASE(false, true, false, 0)
+#undef FLEXQ_T6_CASE
+}
+
+constexpr int64_t kT6TokChunk = 64;  // 8 mma n-tiles per launch
+
+static int64_t ws_counters_offset(int64_t ksplit, int64_t m_pad, int64_t rt) {
+  const int64_t mc = m_pad < kT6TokChunk ? m_pad : kT6TokChunk;
+  return cdiv(ksplit * mc * rt * kRowTile * 4, 256) * 256;
+}
+
+int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int ksplit) {
+  T6Geom G(n, k, gs);
+  if (ksplit <= 0) ksplit = auto_ksplit_t6(G.rt, G.kb);
+  const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
+  return ws_counters_offset(ksplit, m_pad, G.rt) + cdiv(G.rt * 4, 256) * 256;
+}
+
+int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
+                   const uint32_t* act_frag, const float* act_scale, const int32_t* act_corr,
+                   int64_t m, int64_t m_pad, int64_t n, int64_t k, int64_t gs, int32_t* partials,
+                   void* y, int out_dtype, void* workspace, int ksplit, cudaStream_t st) {
+  if (m < 1 || n < 1 || k < 1 || gs < 1) {
+    set_error("gemm_t6: dims must be positive, got m=%lld n=%lld k=%lld group=%lld",
+              (long long)m, (long long)n, (long long)k, (long long)gs);
+    return FLEXQ_ERR_CONFIG;
+  }
+  if (m_pad < m || m_pad % kTokTile) {
+    set_error("gemm_t6: m_pad (%lld) must be a multiple of 8 >= m (%lld)", (long long)m_pad,
+              (long long)m);
+    return FLEXQ_ERR_SHAPE;
+  }
+  if (out_dtype != FLEXQ_OUT_F16 && out_dtype != FLEXQ_OUT_F32) {
+    set_error("gemm_t6: unknown out_dtype %d", out_dtype);
+    return FLEXQ_ERR_CONFIG;
+  }
+  const bool fast = y != nullptr, trace = partials != nullptr;
+  if (!fast && !trace) {
+    set_error("gemm_t6: nothing to compute (y and partials are both NULL)");
+    return FLEXQ_ERR_CONFIG;
+  }
+  T6Geom G(n, k, gs);
+  if (ksplit <= 0) ksplit = auto_ksplit_t6(G.rt, G.kb);
+  if (ksplit > 65535) ksplit = 65535;
+  if (ksplit > 1 && fast && !workspace) {
+    set_error("gemm_t6: workspace required for ksplit=%d", ksplit);
+    return FLEXQ_ERR_CONFIG;
+  }
+  for (int64_t m0 = 0; m0 < m; m0 += kT6TokChunk) {
+    const int64_t mc = (m - m0) < kT6TokChunk ? (m - m0) : kT6TokChunk;
+    T6Params p;
+    p.t6 = reinterpret_cast<const uint4*>(t6);
+    p.wscale = wscale;
+    p.act = reinterpret_cast<const uint4*>(act_frag) + (m0 / kTokTile) * G.kb * 32 * 2;
+    p.xs = act_scale + m0;
+    p.corr = act_corr + m0;
+    p.m = mc;
+    p.m_pad = m_pad;
+    p.n = n;
+    p.m_total = m;
+    p.tok0 = m0;
+    p.ws_mstride = cdiv(mc, kTokTile) * kTokTile;
+    p.ng = G.ng; p.spg = G.spg; p.ks = G.ks; p.kb = G.kb; p.rt = G.rt;
+    p.partials = partials;
+    p.y = y;
+    p.ws_part = reinterpret_cast<float*>(workspace);
+    p.counters = workspace ? reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) +
+                                                         ws_counters_offset(ksplit, m_pad, G.rt))
+                           : nullptr;
+    p.ksplit = ksplit;
+    const int mtiles = (int)cdiv(mc, kTokTile);
+    if (mtiles <= 1) dispatch_t6<1>(p, scale_f16, trace, fast, out_dtype, st);
+    else if (mtiles <= 2) dispatch_t6<2>(p, scale_f16, trace, fast, out_dtype, st);
+    else if (mtiles <= 4) dispatch_t6<4>(p, scale_f16, trace, fast, out_dtype, st);
+    else dispatch_t6<8>(p, scale_f16, trace, fast, out_dtype, st);
+    FLEXQ_LAUNCH_CHECK("gemm_t6");
+  }
+  return FLEXQ_OK;
+}
+
+}  // namespace flexq

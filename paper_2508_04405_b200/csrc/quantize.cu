@@ -1,0 +1,306 @@
+// Symmetric per-(row, group) quantizer -- the online activation quantizer of
+// the hot path and the offline weight quantizer.
+//
+// Follows quantize.py:118-148 exactly: scale = max|x| / qmax in float64
+// (1.0 for an all-zero group, quantize.py:99-110), optionally rounded to fp16
+// straight from float64 (quantize.py:143-144), code = clamp(sign(v) *
+// floor(|v| + 0.5), +-qmax) with v = x / scale in float64 (quantize.py:29-31,
+// 147).  Every step is one correctly-rounded IEEE float64 operation, so the
+// codes and scales are bit-identical with numpy for every input dtype.
+//
+// One warp owns one (row, group) for groups up to kWarpGroupMax elements; a
+// whole CTA owns it for larger groups (per-token mode, group_size >= K).
+// Besides row-major codes / float64 scales (the QuantTensor of the drop-in
+// API) it can emit, fused, the i8-path activation operand: codes scattered
+// into the T6 B-fragment layout, fp32 scales and the offset-binary correction
+// 32 * sum(codes) per (group, token).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace flexq {
+
+template <int DT>
+__device__ __forceinline__ double load_as_f64(const void* base, int64_t i) {
+  if constexpr (DT == FLEXQ_DT_F16) {
+    return (double)__half2float(reinterpret_cast<const __half*>(base)[i]);
+  } else if constexpr (DT == FLEXQ_DT_BF16) {
+    return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[i]);
+  } else if constexpr (DT == FLEXQ_DT_F32) {
+    return (double)reinterpret_cast<const float*>(base)[i];
+  } else {
+    return reinterpret_cast<const double*>(base)[i];
+  }
+}
+
+struct QuantArgs {
+  const void* x;
+  int64_t rows, cols, gs, ng;
+  int bits;
+  int fp16_scales;
+  int8_t* codes;
+  double* scales;
+  uint8_t* act_frag;
+  float* act_scale;
+  int32_t* act_corr;
+  int64_t m_pad;
+  uint32_t* flag;
+  // T6 geometry of the activation fragment layout
+  int64_t spg, kb;
+};
+
+__device__ __forceinline__ double group_scale(double peak, int bits, int fp16, uint32_t* flag) {
+  const double lim = (double)((1 << (bits - 1)) - 1);
+  double s = peak > 0.0 ? peak / lim : 1.0;
+  if (fp16) s = (double)__half2float(__double2half(s));
+  if (!(s > 0.0) && flag) atomicOr(flag, FLEXQ_FLAG_NONPOS_SCALE);
+  return s;
+}
+
+__device__ __forceinline__ int quant_one(double v, double s, int bits) {
+  const double lim = (double)((1 << (bits - 1)) - 1);
+  double q = v / s;
+  double a = floor(fabs(q) + 0.5);
+  if (a > lim) a = lim;
+  return q < 0.0 ? -(int)a : (int)a;
+}
+
+__device__ __forceinline__ int64_t frag_byte(const QuantArgs& A, int64_t m, int64_t c) {
+  const int64_t g = c / A.gs, j = c - g * A.gs;
+  const int64_t kp = g * A.spg * kKStep + j;
+  const int64_t ks = kp >> 5, within = kp & 31;
+  const int64_t kb = ks >> 2, jj = ks & 3;
+  const int64_t half = within >> 4, wi = within & 15;
+  const int64_t t = wi >> 2, byte = wi & 3;
+  const int64_t lane = (m & 7) * 4 + t, mt = m >> 3;
+  const int64_t word = ((mt * A.kb + kb) * 32 + lane) * 8 + 2 * jj + half;
+  return word * 4 + byte;
+}
+
+__device__ __forceinline__ void emit(const QuantArgs& A, int64_t r, int64_t c, int code) {
+  if (A.codes) A.codes[r * A.cols + c] = (int8_t)code;
+  if (A.act_frag) A.act_frag[frag_byte(A, r, c)] = (uint8_t)(int8_t)code;
+}
+
+// ---- warp per (row, group) ---------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(256) quantize_warp_kernel(QuantArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= A.rows * A.ng) return;
+  const int64_t r = item / A.ng, g = item - r * A.ng;
+  const int64_t lo = g * A.gs, hi = min(lo + A.gs, A.cols);
+  const int64_t base = r * A.cols;
+  double peak = 0.0;
+  bool finite = true;
+  for (int64_t c = lo + lane; c < hi; c += 32) {
+    double v = load_as_f64<DT>(A.x, base + c);
+    finite &= isfinite(v);
+    peak = fmax(peak, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+  if (!__all_sync(0xffffffffu, finite)) {
+    if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
+    peak = 0.0;  // keep going deterministically; the wrapper raises
+  }
+  const double s = group_scale(peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
+  int csum = 0;
+  for (int64_t c = lo + lane; c < hi; c += 32) {
+    double v = load_as_f64<DT>(A.x, base + c);
+    int code = isfinite(v) ? quant_one(v, s, A.bits) : 0;
+    csum += code;
+    emit(A, r, c, code);
+  }
+  if (lane == 0 && A.scales) A.scales[r * A.ng + g] = s;
+  if (A.act_scale || A.act_corr) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if (lane == 0) {
+      if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)s;
+      if (A.act_corr) A.act_corr[g * A.m_pad + r] = 32 * csum;
+    }
+  }
+}
+
+// ---- CTA per (row, group): large groups (per-token / per-channel mode) -------
+template <int DT>
+__global__ void __launch_bounds__(1024) quantize_cta_kernel(QuantArgs A) {
+  __shared__ double red_d[32];
+  __shared__ int red_i[32];
+  __shared__ int red_f[32];
+  const int64_t r = blockIdx.x / A.ng, g = blockIdx.x - r * A.ng;
+  const int64_t lo = g * A.gs, hi = min(lo + A.gs, A.cols);
+  const int64_t base = r * A.cols;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double peak = 0.0;
+  int finite = 1;
+  for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+    double v = load_as_f64<DT>(A.x, base + c);
+    finite &= isfinite(v) ? 1 : 0;
+    peak = fmax(peak, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+  finite = __all_sync(0xffffffffu, finite);
+  if (lane == 0) { red_d[warp] = peak; red_f[warp] = finite; }
+  __syncthreads();
+  if (warp == 0) {
+    peak = lane < nw ? red_d[lane] : 0.0;
+    finite = lane < nw ? red_f[lane] : 1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    finite = __all_sync(0xffffffffu, finite);
+    if (lane == 0) {
+      if (!finite) { atomicOr(A.flag, FLEXQ_FLAG_NONFINITE); peak = 0.0; }
+      red_d[0] = group_scale(peak, A.bits, A.fp16_scales, A.flag);
+    }
+  }
+  __syncthreads();
+  const double s = red_d[0];
+  int csum = 0;
+  for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+    double v = load_as_f64<DT>(A.x, base + c);
+    int code = isfinite(v) ? quant_one(v, s, A.bits) : 0;
+    csum += code;
+    emit(A, r, c, code);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  __syncthreads();
+  if (lane == 0) red_i[warp] = csum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < nw; w++) tot += red_i[w];
+    if (A.scales) A.scales[r * A.ng + g] = s;
+    if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)s;
+    if (A.act_corr) A.act_corr[g * A.m_pad + r] = 32 * tot;
+  }
+}
+
+// ---- already-quantized codes -> T6 activation operand (warp per (row, group)) -----
+// Used when the caller holds a QuantTensor (int_matmul_reference semantics,
+// engine.py:337-365) instead of float activations.
+__global__ void __launch_bounds__(256) codes_to_frag_kernel(QuantArgs A,
+                                                            const int8_t* __restrict__ codes,
+                                                            const double* __restrict__ scales) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= A.rows * A.ng) return;
+  const int64_t r = item / A.ng, g = item - r * A.ng;
+  const int64_t lo = g * A.gs, hi = min(lo + A.gs, A.cols);
+  int csum = 0;
+  for (int64_t c = lo + lane; c < hi; c += 32) {
+    const int code = codes[r * A.cols + c];
+    csum += code;
+    A.act_frag[frag_byte(A, r, c)] = (uint8_t)(int8_t)code;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  if (lane == 0) {
+    A.act_scale[g * A.m_pad + r] = (float)scales[r * A.ng + g];
+    A.act_corr[g * A.m_pad + r] = 32 * csum;
+  }
+}
+
+int codes_to_frag_launch(const int8_t* codes, const double* scales, int64_t m, int64_t m_pad,
+                         int64_t k, int64_t gs, uint32_t* act_frag, float* act_scale,
+                         int32_t* act_corr, cudaStream_t st) {
+  if (m < 1 || k < 1 || gs < 1 || m_pad < m || m_pad % kTokTile) {
+    set_error("pack_act_t6: bad geometry m=%lld m_pad=%lld k=%lld group=%lld", (long long)m,
+              (long long)m_pad, (long long)k, (long long)gs);
+    return FLEXQ_ERR_SHAPE;
+  }
+  T6Geom geo(m_pad, k, gs);
+  QuantArgs A{nullptr, m, k, gs, geo.ng, 8, 0, nullptr, nullptr,
+              reinterpret_cast<uint8_t*>(act_frag), act_scale, act_corr, m_pad, nullptr,
+              geo.spg, geo.kb};
+  codes_to_frag_kernel<<<(unsigned)cdiv(m * geo.ng, 8), 256, 0, st>>>(A, codes, scales);
+  FLEXQ_LAUNCH_CHECK("pack_act_t6");
+  return FLEXQ_OK;
+}
+
+// ---- sum(popcount(a & b)) over a byte span (bmma_chunk, engine.py:89-95) ----------
+__global__ void popcount_and_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
+                                    int64_t nbytes, unsigned long long* out) {
+  unsigned long long tot = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbytes;
+       i += (int64_t)gridDim.x * blockDim.x)
+    tot += __popc((unsigned)(a[i] & b[i]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(out, tot);
+}
+
+int popcount_and_launch(const uint8_t* a, const uint8_t* b, int64_t nbytes, int64_t* out,
+                        cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int64_t), st);
+  if (e != cudaSuccess) return cuda_status(e, "popcount_and");
+  if (nbytes > 0) {
+    const int64_t blocks = cdiv(nbytes, 256) < 1024 ? cdiv(nbytes, 256) : 1024;
+    popcount_and_kernel<<<(unsigned)blocks, 256, 0, st>>>(
+        a, b, nbytes, reinterpret_cast<unsigned long long*>(out));
+    FLEXQ_LAUNCH_CHECK("popcount_and");
+  }
+  return FLEXQ_OK;
+}
+
+constexpr int64_t kWarpGroupMax = 1024;
+
+template <int DT>
+static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
+  const int64_t items = A.rows * A.ng;
+  if (A.gs <= kWarpGroupMax || A.cols <= kWarpGroupMax) {
+    const int warps = 8;
+    quantize_warp_kernel<DT><<<(unsigned)cdiv(items, warps), warps * 32, 0, st>>>(A);
+  } else {
+    quantize_cta_kernel<DT><<<(unsigned)items, 1024, 0, st>>>(A);
+  }
+}
+
+int quantize_launch(const void* x, int dtype, int64_t rows, int64_t cols, int bits, int64_t gs,
+                    int fp16_scales, int8_t* codes, double* scales, uint32_t* act_frag,
+                    float* act_scale, int32_t* act_corr, int64_t m_pad, uint32_t* flag,
+                    cudaStream_t st) {
+  if (rows < 1 || cols < 1) {
+    set_error("quantize: expected a non-empty 2-D tensor, got (%lld, %lld)", (long long)rows,
+              (long long)cols);
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  if (bits < 2 || bits > 8) {
+    set_error("bits must be in 2..8, got %d", bits);
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  if (gs < 1) {
+    set_error("group_size must be >= 1, got %lld", (long long)gs);
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  if (!flag) {
+    set_error("quantize: flag pointer is required");
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  const bool frag = act_frag || act_scale || act_corr;
+  if (frag && (m_pad < rows || m_pad % kTokTile)) {
+    set_error("quantize: m_pad (%lld) must be a multiple of 8 >= rows (%lld)", (long long)m_pad,
+              (long long)rows);
+    return FLEXQ_ERR_SHAPE;
+  }
+  T6Geom geo(m_pad > 0 ? m_pad : rows, cols, gs);
+  QuantArgs A{x, rows, cols, gs, geo.ng, bits, fp16_scales, codes, scales,
+              reinterpret_cast<uint8_t*>(act_frag), act_scale, act_corr, m_pad, flag,
+              geo.spg, geo.kb};
+  switch (dtype) {
+    case FLEXQ_DT_F16: launch_quantize<FLEXQ_DT_F16>(A, st); break;
+    case FLEXQ_DT_BF16: launch_quantize<FLEXQ_DT_BF16>(A, st); break;
+    case FLEXQ_DT_F32: launch_quantize<FLEXQ_DT_F32>(A, st); break;
+    case FLEXQ_DT_F64: launch_quantize<FLEXQ_DT_F64>(A, st); break;
+    default:
+      set_error("quantize: unknown dtype code %d", dtype);
+      return FLEXQ_ERR_INVALID_INPUT;
+  }
+  FLEXQ_LAUNCH_CHECK("quantize");
+  return FLEXQ_OK;
+}
+
+}  // namespace flexq

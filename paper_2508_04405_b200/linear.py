@@ -1,0 +1,100 @@
+"""FlexQLinear: the production W6A6/W6A8 linear layer on the B200.
+
+The reference's quantized_linear (engine.py:487-513) re-quantizes and
+re-packs the weights on every call.  Here the offline half (INT6 weight
+quantization + T6 packing) runs once at construction, and each forward is the
+online half only: fused per-token/per-group activation quantizer -> T6
+tensor-core GEMV/GEMM with the fused fp32 group-dequant epilogue -> fp16 out.
+Both kernels run back to back on the caller's stream through one C-ABI call
+(flexq_linear_forward); buffers are preallocated per batch size so the call
+never allocates and can be captured in a CUDA graph.
+"""
+from __future__ import annotations
+
+from . import _dev, _lib
+from .errors import InvalidInputError, ShapeError
+from .quantize import DEFAULT_GROUP_SIZE, DEFAULT_POLICY, BitPolicy, quantize
+from .quantize import activation_bits as policy_bits
+
+
+class FlexQLinear:
+    """y = dequant(Q6(W)) applied to Q_q(x), fp16 in / fp16 out.
+
+    weight: [N, K] float (numpy or torch).  ``activation_bits`` may be given
+    directly or resolved from ``layer_kind`` under ``policy`` (A8 for down_proj
+    in the default FlexQ policy, quantize.py:172-198).  ``fp16_scales`` stores
+    the weight scales in fp16 (the kernel's 2 bytes/group; bit-exact with the
+    reference's fp16-scale mode).
+    """
+
+    def __init__(self, weight, weight_bits: int = 6, activation_bits: int | None = None,
+                 group_size: int = DEFAULT_GROUP_SIZE, fp16_scales: bool = True,
+                 layer_kind: str | None = None, policy: BitPolicy = DEFAULT_POLICY):
+        if weight_bits > 6:
+            raise InvalidInputError(f"FlexQLinear packs at most 6-bit weights, got {weight_bits}")
+        if activation_bits is None:
+            activation_bits = policy_bits(layer_kind or "generic", policy)
+        t = _dev.torch()
+        self.weight_bits = weight_bits
+        self.activation_bits = int(activation_bits)
+        self.group_size = int(group_size)
+        self.fp16_scales = bool(fp16_scales)
+        self.layer_kind = layer_kind
+        self.qweight = quantize(weight if _dev.is_torch(weight) else _dev.to_device(weight),
+                                weight_bits, group_size, fp16_scales=fp16_scales)
+        codes, scales = self.qweight.device_tensors()
+        self.n, self.k = codes.shape
+        from .engine import t6_pack_weights
+
+        self.t6, self.wscale = t6_pack_weights(codes, scales, self.k, self.group_size,
+                                               scale_f16=self.fp16_scales)
+        self.device = codes.device
+        self._bufs: dict[int, tuple] = {}
+        self.flag = t.zeros(1, dtype=t.int32, device=self.device)
+
+    # -- buffers ------------------------------------------------------------------------
+    def buffers(self, m: int):
+        if m not in self._bufs:
+            t = _dev.torch()
+            L = _lib.lib()
+            act = t.empty(L.flexq_act_buf_bytes(m, self.k, self.group_size), dtype=t.uint8,
+                          device=self.device)
+            ws = t.zeros(max(L.flexq_gemm_workspace_bytes(m, self.n, self.k, self.group_size, 0), 16),
+                         dtype=t.uint8, device=self.device)
+            self._bufs[m] = (act, ws)
+        return self._bufs[m]
+
+    @property
+    def weight_bytes(self) -> int:
+        """Bytes of packed weights + scales streamed per call."""
+        return self.t6.numel() * 4 + self.wscale.numel() * self.wscale.element_size()
+
+    # -- forward --------------------------------------------------------------------------
+    def forward(self, x, out=None):
+        """x: fp16 CUDA [M, K] -> fp16 CUDA [M, N] (no host sync)."""
+        t = _dev.torch()
+        if x.dim() != 2 or x.shape[1] != self.k:
+            raise ShapeError(f"activation shape {tuple(x.shape)} does not match K={self.k}")
+        if x.dtype != t.float16:
+            x = x.to(t.float16)
+        x = x.contiguous()
+        m = x.shape[0]
+        if out is None:
+            out = t.empty((m, self.n), dtype=t.float16, device=self.device)
+        act, ws = self.buffers(m)
+        _lib.check(_lib.lib().flexq_linear_forward(
+            _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), self.activation_bits,
+            _lib.ptr(x), m, self.n, self.k, self.group_size, _lib.ptr(out), _lib.ptr(act),
+            _lib.ptr(ws), _lib.ptr(self.flag), _lib.stream()))
+        return out
+
+    __call__ = forward
+
+    def check_errors(self) -> None:
+        """Raise if any forward since the last check saw non-finite input (host sync)."""
+        bits = int(self.flag.item())
+        self.flag.zero_()
+        if bits & _lib.FLAG_NONFINITE:
+            raise InvalidInputError("input contains non-finite values")
+        if bits & _lib.FLAG_NONPOS_SCALE:
+            raise InvalidInputError("all scales must be strictly positive")
