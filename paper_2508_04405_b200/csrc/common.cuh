@@ -23,6 +23,8 @@ constexpr int kKStep = 32;     // mma.m16n8k32 contraction per instruction
 constexpr int kStepsPerBlock = 4;  // one T6 k-block = 4 k-steps = 128 k-slots
 constexpr int kRowTile = 16;   // mma M (weight rows per A fragment)
 constexpr int kTokTile = 8;    // mma N (tokens per B fragment)
+constexpr int kRowGroup = 4;   // row tiles per T6 unit (64 weight rows share one B fragment)
+constexpr int kUnitBytes = kRowGroup * 3 * 512;  // T6 bytes per (row group, k-block) unit
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -34,13 +36,34 @@ struct T6Geom {
   int64_t spg;  // k-steps per group
   int64_t ks;   // total k-steps = ng * spg
   int64_t kb;   // k-blocks = ceil(ks / 4)
-  int64_t rt;   // row tiles = ceil(n / 16)
+  int64_t rg;   // row groups = ceil(n / 64)
+  int64_t rt;   // row tiles = 4 * rg (rows padded to 64)
+  __host__ __device__ T6Geom() : n(0), k(0), gs(1), ng(0), spg(1), ks(0), kb(0), rg(0), rt(0) {}
   __host__ __device__ T6Geom(int64_t n_, int64_t k_, int64_t gs_) : n(n_), k(k_), gs(gs_) {
     ng = cdiv(k, gs);
     spg = cdiv(gs < k ? gs : k, kKStep);  // a group holds at most min(gs, k) elements
     ks = ng * spg;
     kb = cdiv(ks, kStepsPerBlock);
-    rt = cdiv(n, kRowTile);
+    rg = cdiv(n, kRowTile * kRowGroup);
+    rt = rg * kRowGroup;
+  }
+  // uint4 index of T6 vector v (0: L0, 1: L1, 2: H) of `lane` for (row tile, k-block):
+  // layout [rg][kb][r][v][lane] x 16 B, i.e. unit u = rg*kb_total + kb is 6 KB contiguous
+  __host__ __device__ int64_t vec_index(int64_t rtile, int64_t kblk, int v, int lane) const {
+    const int64_t g = rtile / kRowGroup, r = rtile - g * kRowGroup;
+    return (((g * kb + kblk) * kRowGroup + r) * 3 + v) * 32 + lane;
+  }
+  // half2/float2 index of the weight-scale pair {row 16rt+gq, row 16rt+gq+8} of group `grp`:
+  // layout [rg][G][r][8] pairs (128 B of fp16 per (row group, group))
+  __host__ __device__ int64_t scale_index(int64_t rtile, int64_t grp, int gq) const {
+    const int64_t g = rtile / kRowGroup, r = rtile - g * kRowGroup;
+    return ((g * ng + grp) * kRowGroup + r) * 8 + gq;
+  }
+  // u32 word index inside the activation fragment array [mt][kb][c][lane][4 words]:
+  // chunk c = jj/2, word w = (jj%2)*2 + half  (half 0 = b0, 1 = b1 of k-step jj)
+  __host__ __device__ static int64_t act_word(int64_t kb_total, int64_t mt, int64_t kblk, int jj,
+                                             int half, int lane) {
+    return ((mt * kb_total + kblk) * 2 + (jj >> 1)) * 128 + lane * 4 + (jj & 1) * 2 + half;
   }
   // padded slot of logical column kk
   __host__ __device__ int64_t slot(int64_t kk) const {
@@ -48,5 +71,102 @@ struct T6Geom {
     return g * spg * kKStep + j;
   }
 };
+
+// ---- async-copy / mbarrier primitives (sm_90+ PTX, used by the TMA-fed kernels) ----------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---- T6 unpack + IMMA -------------------------------------------------------------------
+// A registers of one m16n8k32 from the three T6 words of a k-step.
+// Offset-binary u = w + 32 in [1, 63] (6 bits).  Byte b of word v holds u(a_v, b) in
+// bits 0-5 and, in bits 6-7, two of the six bits of u(a_3, b): bits 0-1 in W0, 2-3 in
+// W1, 4-5 in W2.  a0..a2 are one AND each; a3 is reassembled with 3 shifts + 3 LOP3.
+__device__ __forceinline__ void unpack_t6(uint32_t W0, uint32_t W1, uint32_t W2, uint32_t a[4]) {
+  a[0] = W0 & 0x3F3F3F3Fu;
+  a[1] = W1 & 0x3F3F3F3Fu;
+  a[2] = W2 & 0x3F3F3F3Fu;
+  const uint32_t lo = ((W0 >> 6) & 0x03030303u) | ((W1 >> 4) & 0x0C0C0C0Cu);
+  a[3] = lo | ((W2 >> 2) & 0x30303030u);
+}
+
+__device__ __forceinline__ void mma_u8s8(int c[4], const uint32_t a[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// same with a zero accumulator input (first k-step of a group)
+__device__ __forceinline__ void mma_u8s8_zc(int c[4], const uint32_t a[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};\n"
+      : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0));
+}
+
+// split-K handshake: release this thread's prior writes / acquire the others'
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ uint32_t u4get(const uint4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
 
 }  // namespace flexq

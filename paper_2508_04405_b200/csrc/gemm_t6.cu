@@ -40,27 +40,13 @@ struct T6Params {
   int64_t m_total, tok0;        // trace / output token indexing
   int64_t ws_mstride;           // token stride of the split-K workspace
   int64_t ng, spg, ks, kb, rt;
+  T6Geom geo;
   int32_t* partials;
   void* y;
   float* ws_part;
   unsigned* counters;
   int ksplit;
 };
-
-__device__ __forceinline__ void unpack_t6(uint32_t L0, uint32_t L1, uint32_t H, uint32_t a[4]) {
-  a[0] = (L0 & 0x0F0F0F0Fu) | ((H & 0x03030303u) << 4);
-  a[1] = ((L0 >> 4) & 0x0F0F0F0Fu) | ((H & 0x0C0C0C0Cu) << 2);
-  a[2] = (L1 & 0x0F0F0F0Fu) | (H & 0x30303030u);
-  a[3] = ((L1 >> 4) & 0x0F0F0F0Fu) | ((H >> 2) & 0x30303030u);
-}
-
-__device__ __forceinline__ void mma_u8s8(int c[4], const uint32_t a[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 
 // Weights are read exactly once: bypass L1 and mark the L2 lines evict-first
 // (the paper's evict_first hint) so the L2-resident
@@ -77,10 +63,6 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p), "l"(pol));
   return r;
-}
-
-__device__ __forceinline__ uint32_t u4get(const uint4& v, int i) {
-  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
 template <bool SF16>
@@ -133,7 +115,7 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
       }
     }
     if constexpr (FAST) {
-      const float2 sw = load_wscale<SF16>(p.wscale, (rt * p.ng + g) * 8 + gq);
+      const float2 sw = load_wscale<SF16>(p.wscale, p.geo.scale_index(rt, g, gq));
 #pragma unroll
       for (int mt = 0; mt < MT; mt++) {
         const float2 sx = *reinterpret_cast<const float2*>(&p.xs[g * p.m_pad + mt * kTokTile + 2 * t]);
@@ -145,12 +127,12 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
     }
   };
 
-  const uint4* wbase = p.t6 + rt * p.kb * 3 * 32 + lane;
+  const uint4* wbase = p.t6 + p.geo.vec_index(rt, 0, 0, lane);
   const uint64_t pol = evict_first_policy();
   int64_t kb = kb0 + warp;
   uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0, w2 = w0;
   if (kb < kb1) {
-    const uint4* q = wbase + kb * 96;
+    const uint4* q = wbase + kb * (kRowGroup * 96);
     w0 = ld_stream(q, pol); w1 = ld_stream(q + 32, pol); w2 = ld_stream(q + 64, pol);
   }
   for (; kb < kb1; kb += kT6Warps) {
@@ -158,15 +140,15 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
     uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0, n2 = n0;
     const int64_t kbn = kb + kT6Warps;
     if (kbn < kb1) {
-      const uint4* q = wbase + kbn * 96;
+      const uint4* q = wbase + kbn * (kRowGroup * 96);
       n0 = ld_stream(q, pol); n1 = ld_stream(q + 32, pol); n2 = ld_stream(q + 64, pol);
     }
     uint4 b[MT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; mt++) {
       if (mt * kTokTile + gq < p.m) {
-        const uint4* q = p.act + ((mt * p.kb + kb) * 32 + lane) * 2;
-        b[mt][0] = __ldg(q); b[mt][1] = __ldg(q + 1);
+        const uint4* q = p.act + ((mt * p.kb + kb) * 2) * 32 + lane;
+        b[mt][0] = __ldg(q); b[mt][1] = __ldg(q + 32);
       } else {
         b[mt][0] = make_uint4(0, 0, 0, 0); b[mt][1] = b[mt][0];
       }
@@ -299,11 +281,22 @@ static int64_t ws_counters_offset(int64_t ksplit, int64_t m_pad, int64_t rt) {
   return cdiv(ksplit * mc * rt * kRowTile * 4, 256) * 256;
 }
 
+bool gemv_stream_supported(int64_t m, int64_t spg);
+int64_t gemv_stream_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
+int gemv_stream_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
+                       const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
+                       int, void*, cudaStream_t);
+
 int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int ksplit) {
   T6Geom G(n, k, gs);
-  if (ksplit <= 0) ksplit = auto_ksplit_t6(G.rt, G.kb);
+  const int ks_eff = ksplit <= 0 ? auto_ksplit_t6(G.rt, G.kb) : ksplit;
   const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
-  return ws_counters_offset(ksplit, m_pad, G.rt) + cdiv(G.rt * 4, 256) * 256;
+  int64_t bytes = ws_counters_offset(ks_eff, m_pad, G.rt) + cdiv(G.rt * 4, 256) * 256;
+  if (ksplit <= 0 && gemv_stream_supported(m, G.spg)) {
+    const int64_t b2 = gemv_stream_workspace(m, n, k, gs);
+    if (b2 > bytes) bytes = b2;
+  }
+  return bytes;
 }
 
 int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
@@ -330,6 +323,10 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
     return FLEXQ_ERR_CONFIG;
   }
   T6Geom G(n, k, gs);
+  // decode regime: the persistent TMA-fed streaming kernel (gemv_stream.cu)
+  if (ksplit <= 0 && gemv_stream_supported(m, G.spg) && (workspace || !fast))
+    return gemv_stream_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
+                              gs, partials, y, out_dtype, workspace, st);
   if (ksplit <= 0) ksplit = auto_ksplit_t6(G.rt, G.kb);
   if (ksplit > 65535) ksplit = 65535;
   if (ksplit > 1 && fast && !workspace) {
@@ -338,7 +335,8 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   }
   for (int64_t m0 = 0; m0 < m; m0 += kT6TokChunk) {
     const int64_t mc = (m - m0) < kT6TokChunk ? (m - m0) : kT6TokChunk;
-    T6Params p;
+    T6Params p{};
+    p.geo = G;
     p.t6 = reinterpret_cast<const uint4*>(t6);
     p.wscale = wscale;
     p.act = reinterpret_cast<const uint4*>(act_frag) + (m0 / kTokTile) * G.kb * 32 * 2;

@@ -7,9 +7,9 @@
 //    word `it` -- the intra-warp bit gather of the paper.
 // 2. The inverse (packing.py:150-165 + bitplane.py:87-89).
 // 3. The T6 layout of the production unpack-to-INT8 path:
-//    offset-binary u = code + 32 split into the low-nibble planes {0..3} and
-//    the high planes {4,5}, ordered so each lane's three 16-byte loads per
-//    k-block are its m16n8k32 A fragments for 4 k-steps.
+//    offset-binary u = code + 32 (6 bits) packed 4 per 3 bytes per lane, so each
+//    lane's three 16-byte loads per k-block are its m16n8k32 A fragments for 4
+//    k-steps (byte layout: unpack_t6 in common.cuh).
 #include "common.cuh"
 
 namespace flexq {
@@ -62,7 +62,7 @@ __global__ void unpack_planes_kernel(const uint8_t* __restrict__ words, int64_t 
 }
 
 // ---- 3. T6 pack --------------------------------------------------------------------
-// thread = (row tile, k-block, lane) -> 12 u32: [v=0 L0 | v=1 L1 | v=2 H] x 4 k-steps
+// thread = (row tile, k-block, lane) -> 12 u32: [v = 0, 1, 2] x 4 k-steps, see unpack_t6
 __global__ void pack_t6_kernel(const int8_t* __restrict__ codes, T6Geom G,
                                uint32_t* __restrict__ t6) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -75,7 +75,7 @@ __global__ void pack_t6_kernel(const int8_t* __restrict__ codes, T6Geom G,
   uint32_t out[3][4];
 #pragma unroll
   for (int jj = 0; jj < 4; jj++) {
-    uint32_t L0 = 0, L1 = 0, H = 0;
+    uint32_t Wv[3] = {0u, 0u, 0u};
     const int64_t ks = kb * 4 + jj;
 #pragma unroll
     for (int reg = 0; reg < 4; reg++) {
@@ -88,37 +88,40 @@ __global__ void pack_t6_kernel(const int8_t* __restrict__ codes, T6Geom G,
         uint32_t u = 0;  // zero padding: contributes nothing whatever the activation
         if (ks < G.ks && g < G.ng && j < G.gs && kk < G.k && row < G.n)
           u = (uint32_t)((int)codes[row * G.k + kk] + 32);
-        const uint32_t lo = u & 15u, hi = u >> 4;
-        if (reg == 0) { L0 |= lo << (8 * b); H |= hi << (8 * b); }
-        if (reg == 1) { L0 |= lo << (8 * b + 4); H |= hi << (8 * b + 2); }
-        if (reg == 2) { L1 |= lo << (8 * b); H |= hi << (8 * b + 4); }
-        if (reg == 3) { L1 |= lo << (8 * b + 4); H |= hi << (8 * b + 6); }
+        if (reg < 3) {
+          Wv[reg] |= u << (8 * b);
+        } else {  // a3: 2 bits into the top of each of the three words
+#pragma unroll
+          for (int v = 0; v < 3; v++) Wv[v] |= ((u >> (2 * v)) & 3u) << (8 * b + 6);
+        }
       }
     }
-    out[0][jj] = L0; out[1][jj] = L1; out[2][jj] = H;
+    out[0][jj] = Wv[0]; out[1][jj] = Wv[1]; out[2][jj] = Wv[2];
   }
 #pragma unroll
   for (int v = 0; v < 3; v++) {
     uint4 val = make_uint4(out[v][0], out[v][1], out[v][2], out[v][3]);
-    reinterpret_cast<uint4*>(t6)[((rt * G.kb + kb) * 3 + v) * 32 + lane] = val;
+    reinterpret_cast<uint4*>(t6)[G.vec_index(rt, kb, v, lane)] = val;
   }
 }
 
-// weight scales for the fast epilogue: [RT, G, 8, 2] = {s[16rt+g], s[16rt+g+8]}
+// weight scales for the fast epilogue: pairs {s[16rt+gq], s[16rt+gq+8]} at
+// T6Geom::scale_index -> [RG, G, 4, 8, 2]
 template <typename T>
 __global__ void pack_t6_scales_kernel(const double* __restrict__ scales, T6Geom G,
                                       T* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= G.rt * G.ng * 16) return;
   const int h = (int)(i & 1), gq = (int)((i >> 1) & 7);
-  const int64_t rg = i >> 4;
-  const int64_t rt = rg / G.ng, g = rg - rt * G.ng;
+  const int64_t q = i >> 4;
+  const int64_t rt = q / G.ng, g = q - rt * G.ng;
   const int64_t row = rt * kRowTile + gq + 8 * h;
   const double s = row < G.n ? scales[row * G.ng + g] : 0.0;
+  const int64_t o = G.scale_index(rt, g, gq) * 2 + h;
   if constexpr (sizeof(T) == 2) {
-    out[i] = __double2half(s);
+    out[o] = __double2half(s);
   } else {
-    out[i] = (float)s;
+    out[o] = (float)s;
   }
 }
 

@@ -73,8 +73,7 @@ __device__ __forceinline__ int64_t frag_byte(const QuantArgs& A, int64_t m, int6
   const int64_t half = within >> 4, wi = within & 15;
   const int64_t t = wi >> 2, byte = wi & 3;
   const int64_t lane = (m & 7) * 4 + t, mt = m >> 3;
-  const int64_t word = ((mt * A.kb + kb) * 32 + lane) * 8 + 2 * jj + half;
-  return word * 4 + byte;
+  return T6Geom::act_word(A.kb, mt, kb, (int)jj, (int)half, (int)lane) * 4 + byte;
 }
 
 __device__ __forceinline__ void emit(const QuantArgs& A, int64_t r, int64_t c, int code) {

@@ -202,7 +202,7 @@ def t6_pack_weights(wcodes, wscales, k: int, group_size: int, scale_f16: bool, w
     ws = None
     if with_scales:
         ng = -(-k // group_size)
-        ws = t.empty(-(-n // 16) * ng * 16, dtype=t.float16 if scale_f16 else t.float32,
+        ws = t.empty(-(-n // 64) * 4 * ng * 16, dtype=t.float16 if scale_f16 else t.float32,
                      device=wcodes.device)
     _lib.check(L.flexq_pack_t6(_lib.ptr(wcodes), _lib.ptr(wscales), n, k, group_size,
                                int(scale_f16), _lib.ptr(t6), _lib.ptr(ws), _lib.stream()))

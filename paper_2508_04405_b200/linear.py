@@ -90,6 +90,29 @@ class FlexQLinear:
 
     __call__ = forward
 
+    def _act_views(self, m: int):
+        """(act_frag, xs, corr) pointers inside the act buffer (mirrors flexq_linear_forward)."""
+        L = _lib.lib()
+        act, _ = self.buffers(m)
+        m_pad = -(-m // 8) * 8
+        ng = -(-self.k // self.group_size)
+        frag = -(-L.flexq_act_frag_bytes(m_pad, self.k, self.group_size) // 256) * 256
+        vec = -(-(ng * m_pad * 4) // 256) * 256
+        base = act.data_ptr()
+        return base, base + frag, base + frag + vec, m_pad
+
+    def gemm_only(self, m: int, out):
+        """Re-run only the T6 GEMM on the activations quantized by the last forward(m).
+
+        Used by bench.py to time the dominant kernel alone (roofline)."""
+        frag, xs, corr, m_pad = self._act_views(m)
+        _, ws = self.buffers(m)
+        _lib.check(_lib.lib().flexq_gemm_t6(
+            _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), frag, xs, corr, m,
+            m_pad, self.n, self.k, self.group_size, None, _lib.ptr(out), _lib.OUT_F16,
+            _lib.ptr(ws), 0, _lib.stream()))
+        return out
+
     def check_errors(self) -> None:
         """Raise if any forward since the last check saw non-finite input (host sync)."""
         bits = int(self.flag.item())

@@ -55,4 +55,31 @@ for (m, n, k, q) in [(1, 4096, 4096, 8), (4, 11008, 4096, 6), (8, 4096, 11008, 8
     bad += not ok
     # trace through the fast kernel
     print("fast", (m, n, k, q), f"maxrel={err:.2e}", ok)
+
+# fast path across group sizes / token counts, plus exact partials through the fast kernel
+from paper_2508_04405_b200.engine import t6_pack_weights, t6_pack_activations
+L = _lib.lib()
+for (m, n, k, q, gs) in [(1, 1000, 1024, 6, 32), (3, 200, 1024, 8, 64), (5, 256, 2048, 6, 256), (2, 512, 4096, 8, 4096),
+                          (16, 384, 896, 6, 128), (12, 130, 640, 8, 100), (9, 1024, 1536, 6, 512), (1, 64, 128, 6, 128)]:
+    w = rng.standard_normal((n, k)).astype(np.float16)
+    x = rng.standard_normal((m, k)).astype(np.float16)
+    wc, wsc = c_oracle.quantize(w, 6, gs, True); xc, xsc = c_oracle.quantize(x, q, gs, True)
+    yr, pr = c_oracle.int_matmul(wc, xc, wsc, xsc, gs, trace=True)
+    dw = torch.from_numpy(wc).cuda(); dws = torch.from_numpy(wsc).cuda()
+    t6, wsp = t6_pack_weights(dw, dws, k, gs, True)
+    frag, xs, corr, m_pad = t6_pack_activations(torch.from_numpy(xc).cuda(), torch.from_numpy(xsc).cuda(), k, gs)
+    ng = -(-k // gs)
+    parts = torch.zeros((ng, m, n), dtype=torch.int32, device="cuda")
+    y = torch.empty((m, n), dtype=torch.float16, device="cuda")
+    wsb = torch.zeros(L.flexq_gemm_workspace_bytes(m, n, k, gs, 0), dtype=torch.uint8, device="cuda")
+    for rep in range(2):
+        parts.zero_()
+        _lib.check(L.flexq_gemm_t6(_lib.ptr(t6), _lib.ptr(wsp), 1, _lib.ptr(frag), _lib.ptr(xs), _lib.ptr(corr), m, m_pad, n, k, gs,
+                                   _lib.ptr(parts), _lib.ptr(y), _lib.OUT_F16, _lib.ptr(wsb), 0, _lib.stream()))
+    torch.cuda.synchronize()
+    pe = np.array_equal(parts.cpu().numpy(), pr)
+    err = np.abs(y.float().cpu().numpy() - yr).max() / np.abs(yr).max()
+    ok = pe and err <= 1e-3
+    bad += not ok
+    print("fast+trace", (m, n, k, q, gs), "partials exact", pe, f"maxrel={err:.2e}")
 print("BAD", bad)
