@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
       const float2 sw = load_wscale<SF16>(p.wscale, p.geo.scale_index(rt, g, gq));
 #pragma unroll
       for (int mt = 0; mt < MT; mt++) {
-        const float2 sx = *reinterpret_cast<const float2*>(&p.xs[g * p.m_pad + mt * kTokTile + 2 * t]);
+        float2 sx = make_float2(0.f, 0.f);  // token tiles past the chunk are never stored
+        if (mt * kTokTile < p.ws_mstride)
+          sx = *reinterpret_cast<const float2*>(&p.xs[g * p.m_pad + mt * kTokTile + 2 * t]);
         acc[mt][0] = fmaf(sw.x * sx.x, (float)P[mt][0], acc[mt][0]);
         acc[mt][1] = fmaf(sw.x * sx.y, (float)P[mt][1], acc[mt][1]);
         acc[mt][2] = fmaf(sw.y * sx.x, (float)P[mt][2], acc[mt][2]);
@@ -165,7 +167,8 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) {
           int2 cr = make_int2(0, 0);
-          if (first) cr = *reinterpret_cast<const int2*>(&p.corr[g * p.m_pad + mt * kTokTile + 2 * t]);
+          if (first && mt * kTokTile < p.ws_mstride)
+            cr = *reinterpret_cast<const int2*>(&p.corr[g * p.m_pad + mt * kTokTile + 2 * t]);
           P[mt][0] = -cr.x; P[mt][1] = -cr.y; P[mt][2] = -cr.x; P[mt][3] = -cr.y;
         }
       }
@@ -207,7 +210,8 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
 #pragma unroll
         for (int i = 0; i < 4; i++) {
           const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = (i & 2) ? row1 : row0;
-          p.ws_part[(split * p.ws_mstride + tok) * n_pad + row] = acc[mt][i];
+          if (tok < p.ws_mstride)  // token tiles past this chunk's padding are not stored
+            p.ws_part[(split * p.ws_mstride + tok) * n_pad + row] = acc[mt][i];
         }
       __threadfence();
       unsigned prev = 0;
@@ -221,7 +225,8 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
         for (int i = 0; i < 4; i++) {
           const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = (i & 2) ? row1 : row0;
           float s = 0.f;
-          for (int sp = 0; sp < p.ksplit; sp++)
+          if (tok < p.ws_mstride)
+            for (int sp = 0; sp < p.ksplit; sp++)
             s += __ldcg(&p.ws_part[(sp * p.ws_mstride + tok) * n_pad + row]);
           acc[mt][i] = s;
         }
