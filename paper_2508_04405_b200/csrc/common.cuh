@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/flexq.h"
 
 namespace flexq {
@@ -71,6 +73,31 @@ struct T6Geom {
     return g * spg * kKStep + j;
   }
 };
+
+// ---- programmatic dependent launch (PDL) -------------------------------------------------
+// Kernels launched with launch_pdl may start while the previous kernel on the stream is
+// still running; pdl_wait() blocks until that grid has completed and its writes are
+// visible (a no-op when there is no programmatic predecessor).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---- async-copy / mbarrier primitives (sm_90+ PTX, used by the TMA-fed kernels) ----------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

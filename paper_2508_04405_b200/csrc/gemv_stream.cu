@@ -122,39 +122,65 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
       return 1;
     }
   };
-  auto issue = [&](int64_t u, int rg, int kb, int g_lo, int s) {
+  // part 0: weights + weight scales (offline data, may run before pdl_wait);
+  // part 1: activation fragments, scales, corrections (written by the quantizer)
+  auto issue = [&](int64_t u, int rg, int kb, int g_lo, int s, int part) {
     const int ngr = group_cnt(kb, g_lo);
     const uint32_t wsb = FAST ? (uint32_t)(ngr * kRowGroup * 8 * SB) : 0u;
     const uint32_t xsb = FAST ? (uint32_t)(ngr * p.m_pad * 4) : 0u;
     const uint32_t cb = (uint32_t)(ngr * p.m_pad * 4);
     uint8_t* dst = ring + s * UB;
-    mbar_expect_tx(&bar[s], kUnitBytes + MT * 1024 + wsb + xsb + cb);
-    bulk_g2s(dst, p.t6 + u * (int64_t)kUnitBytes, kUnitBytes, &bar[s], pol_w);
+    if (part == 0) {
+      mbar_expect_tx(&bar[s], kUnitBytes + MT * 1024 + wsb + xsb + cb);
+      bulk_g2s(dst, p.t6 + u * (int64_t)kUnitBytes, kUnitBytes, &bar[s], pol_w);
+      if (FAST)
+        bulk_g2s(dst + L::kOffWs,
+                 reinterpret_cast<const uint8_t*>(p.wscale) +
+                     p.geo.scale_index(rg * kRowGroup, g_lo, 0) * SB,
+                 wsb, &bar[s], pol_w);
+    } else {
 #pragma unroll
-    for (int mt = 0; mt < MT; mt++)
-      bulk_g2s(dst + L::kOffB + mt * 1024, p.act + ((int64_t)mt * p.kb + kb) * 1024, 1024,
-               &bar[s], pol_a);
-    if (FAST) {
-      bulk_g2s(dst + L::kOffWs,
-               reinterpret_cast<const uint8_t*>(p.wscale) +
-                   p.geo.scale_index(rg * kRowGroup, g_lo, 0) * SB,
-               wsb, &bar[s], pol_w);
-      bulk_g2s(dst + L::kOffXs, p.xs + g_lo * p.m_pad, xsb, &bar[s], pol_a);
+      for (int mt = 0; mt < MT; mt++)
+        bulk_g2s(dst + L::kOffB + mt * 1024, p.act + ((int64_t)mt * p.kb + kb) * 1024, 1024,
+                 &bar[s], pol_a);
+      if (FAST) bulk_g2s(dst + L::kOffXs, p.xs + g_lo * p.m_pad, xsb, &bar[s], pol_a);
+      bulk_g2s(dst + L::kOffCorr, p.corr + g_lo * p.m_pad, cb, &bar[s], pol_a);
     }
-    bulk_g2s(dst + L::kOffCorr, p.corr + g_lo * p.m_pad, cb, &bar[s], pol_a);
   };
   // issue cursor (lane 0 only): next unit to fetch
   int64_t iu = u0;
   int irg = (int)(u0 / p.kb), ikb = (int)(u0 - (int64_t)irg * p.kb);
   int ig = MODE == 2 ? ikb / spu : 0, irem = MODE == 2 ? ikb - ig * spu : 0;
   auto issue_next = [&](int s) {
-    issue(iu, irg, ikb, group_lo(ikb, ig), s);
+    issue(iu, irg, ikb, group_lo(ikb, ig), s, 0);
+    issue(iu, irg, ikb, group_lo(ikb, ig), s, 1);
     iu++;
     if (++ikb == kbn) { ikb = 0; irg++; ig = 0; irem = 0; }
     else if (MODE == 2 && ++irem == spu) { irem = 0; ig++; }
   };
-  if (lane == 0)
-    for (int s = 0; s < S && iu < u1; s++) issue_next(s);
+  // Prologue: start the weight stream, then wait for the quantizer (PDL) before the
+  // activation side of the same stages.
+  int pro = 0;
+  if (lane == 0) {
+    int64_t pu = iu;
+    int prg = irg, pkb = ikb, pg = ig, prem = irem;
+    for (; pro < S && pu < u1; pro++) {
+      issue(pu, prg, pkb, group_lo(pkb, pg), pro, 0);
+      pu++;
+      if (++pkb == kbn) { pkb = 0; prg++; pg = 0; prem = 0; }
+      else if (MODE == 2 && ++prem == spu) { prem = 0; pg++; }
+    }
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+  if (lane == 0) {
+    for (int s = 0; s < pro; s++) {
+      issue(iu, irg, ikb, group_lo(ikb, ig), s, 1);
+      iu++;
+      if (++ikb == kbn) { ikb = 0; irg++; ig = 0; irem = 0; }
+      else if (MODE == 2 && ++irem == spu) { irem = 0; ig++; }
+    }
+  }
 
   float acc[4][MT][4];
   int P[4][MT][4];
@@ -430,8 +456,8 @@ static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
   if (warps > by_units) warps = by_units;
   p.nw = warps;
   const unsigned ctas = (unsigned)cdiv(warps, kSWarps);
-  kern<<<ctas, kSWarps * 32, smem, st>>>(p);
-  FLEXQ_LAUNCH_CHECK("gemv_t6_stream");
+  cudaError_t e = launch_pdl(kern, dim3(ctas), dim3(kSWarps * 32), (size_t)smem, st, p);
+  if (e != cudaSuccess) return cuda_status(e, "gemv_t6_stream launch");
   return FLEXQ_OK;
 }
 

@@ -84,15 +84,26 @@ __device__ __forceinline__ void emit(const QuantArgs& A, int64_t r, int64_t c, i
 // ---- warp per (row, group) ---------------------------------------------------
 template <int DT>
 __global__ void __launch_bounds__(256) quantize_warp_kernel(QuantArgs A) {
+  pdl_wait();               // x may be the previous kernel's output
+  pdl_launch_dependents();  // let the GEMM launch and start streaming its weights
   const int lane = threadIdx.x & 31;
   const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (item >= A.rows * A.ng) return;
   const int64_t r = item / A.ng, g = item - r * A.ng;
   const int64_t lo = g * A.gs, hi = min(lo + A.gs, A.cols);
   const int64_t base = r * A.cols;
+  constexpr int kReg = 8;  // groups up to 256 stay in registers (single pass over x)
+  double vals[kReg];
   double peak = 0.0;
   bool finite = true;
-  for (int64_t c = lo + lane; c < hi; c += 32) {
+#pragma unroll
+  for (int i = 0; i < kReg; i++) {
+    const int64_t c = lo + lane + 32 * i;
+    vals[i] = c < hi ? load_as_f64<DT>(A.x, base + c) : 0.0;
+    finite &= isfinite(vals[i]);
+    peak = fmax(peak, fabs(vals[i]));
+  }
+  for (int64_t c = lo + lane + 32 * kReg; c < hi; c += 32) {  // larger groups: stream the rest
     double v = load_as_f64<DT>(A.x, base + c);
     finite &= isfinite(v);
     peak = fmax(peak, fabs(v));
@@ -105,7 +116,16 @@ __global__ void __launch_bounds__(256) quantize_warp_kernel(QuantArgs A) {
   }
   const double s = group_scale(peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
   int csum = 0;
-  for (int64_t c = lo + lane; c < hi; c += 32) {
+#pragma unroll
+  for (int i = 0; i < kReg; i++) {
+    const int64_t c = lo + lane + 32 * i;
+    if (c < hi) {
+      const int code = isfinite(vals[i]) ? quant_one(vals[i], s, A.bits) : 0;
+      csum += code;
+      emit(A, r, c, code);
+    }
+  }
+  for (int64_t c = lo + lane + 32 * kReg; c < hi; c += 32) {
     double v = load_as_f64<DT>(A.x, base + c);
     int code = isfinite(v) ? quant_one(v, s, A.bits) : 0;
     csum += code;
@@ -125,6 +145,8 @@ __global__ void __launch_bounds__(256) quantize_warp_kernel(QuantArgs A) {
 // ---- CTA per (row, group): large groups (per-token / per-channel mode) -------
 template <int DT>
 __global__ void __launch_bounds__(1024) quantize_cta_kernel(QuantArgs A) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double red_d[32];
   __shared__ int red_i[32];
   __shared__ int red_f[32];
@@ -252,9 +274,10 @@ static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
   const int64_t items = A.rows * A.ng;
   if (A.gs <= kWarpGroupMax || A.cols <= kWarpGroupMax) {
     const int warps = 8;
-    quantize_warp_kernel<DT><<<(unsigned)cdiv(items, warps), warps * 32, 0, st>>>(A);
+    launch_pdl(quantize_warp_kernel<DT>, dim3((unsigned)cdiv(items, warps)), dim3(warps * 32), 0,
+               st, A);
   } else {
-    quantize_cta_kernel<DT><<<(unsigned)items, 1024, 0, st>>>(A);
+    launch_pdl(quantize_cta_kernel<DT>, dim3((unsigned)items), dim3(1024), 0, st, A);
   }
 }
 
