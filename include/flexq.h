@@ -91,6 +91,12 @@ int flexq_pack_t6(const int8_t* codes, const double* scales, int64_t n, int64_t 
                   int64_t group_size, int scale_f16, uint32_t* t6, void* wscale,
                   cudaStream_t stream);
 int64_t flexq_act_frag_bytes(int64_t m_pad, int64_t k, int64_t group_size);
+/* Token padding of the activation operand for m tokens: a multiple of 8 for the
+ * decode GEMV (m <= 16), a whole number of tcgen05 token tiles (32 / 64 / 128)
+ * above.  Layout of the operand: [k-block][m_pad/8][8 k-cores]
+ * [8 tokens][16 B], the K-major no-swizzle UMMA canonical form, read both as
+ * mma.m16n8k32 B fragments and as tcgen05.mma B tiles. */
+int64_t flexq_act_m_pad(int64_t m);
 /* Already-quantized activations (a QuantTensor: int8 codes [m, k] + float64
  * scales [m, G]) -> the T6 activation operand, for int_matmul_reference-style
  * calls (engine.py:337-365) that skip the float quantizer. */
@@ -146,7 +152,7 @@ int flexq_group_epilogue_f64(const int32_t* partials, const double* wscale,
  * Replaces the online half of quantized_linear (engine.py:487-513):
  * quantize activations (fp16 [m, k]) -> T6 GEMM -> fp16 y [m, n].
  * act_buf must hold flexq_act_buf_bytes(); workspace flexq_gemm_workspace_bytes(). */
-int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size);
+int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size);  /* m_pad = flexq_act_m_pad(m) */
 int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
                          const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
                          uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,

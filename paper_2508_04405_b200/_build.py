@@ -8,6 +8,7 @@ statically so the .so only needs the driver on the GPU box.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import shutil
@@ -49,18 +50,37 @@ def needs_rebuild() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(src: str, obj: str) -> subprocess.CompletedProcess:
+    return subprocess.run([nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src], capture_output=True,
+                          text=True)
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per translation unit),
+    then link the shared library."""
     if not force and not needs_rebuild():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
+    obj_dir = os.path.join(OUT_DIR, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
+    srcs = sources()
+    objs = [os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    with concurrent.futures.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        results = list(ex.map(_compile, srcs, objs))
+    failed = False
+    for src, res in zip(srcs, results):
+        if res.returncode != 0:
+            sys.stderr.write(f"--- {os.path.basename(src)}\n" + res.stdout + res.stderr)
+            failed = True
+        elif verbose:
+            sys.stderr.write(res.stderr)
+    if failed:
+        raise RuntimeError("nvcc failed building libflexq_sm100a.so")
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                          "-cudart", "static", "-o", tmp, *objs], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libflexq_sm100a.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libflexq_sm100a.so")
     os.replace(tmp, LIB)
     return LIB
 

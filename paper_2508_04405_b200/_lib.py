@@ -36,6 +36,7 @@ SIGNATURES = {
     "flexq_t6_bytes": (i64, [i64, i64, i64]),
     "flexq_pack_t6": (i32, [vp, vp, i64, i64, i64, i32, vp, vp, vp]),
     "flexq_act_frag_bytes": (i64, [i64, i64, i64]),
+    "flexq_act_m_pad": (i64, [i64]),
     "flexq_pack_act_t6": (i32, [vp, vp, i64, i64, i64, i64, vp, vp, vp, vp]),
     "flexq_gemm_workspace_bytes": (i64, [i64, i64, i64, i64, i32]),
     "flexq_gemm_t6": (i32, [vp, vp, i32, vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, i32, vp, i32, vp]),

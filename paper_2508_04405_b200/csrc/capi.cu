@@ -39,6 +39,7 @@ int gemm_bitserial_launch(const uint8_t*, const uint8_t*, const float*, const fl
 int codes_to_frag_launch(const int8_t*, const double*, int64_t, int64_t, int64_t, int64_t,
                          uint32_t*, float*, int32_t*, cudaStream_t);
 int popcount_and_launch(const uint8_t*, const uint8_t*, int64_t, int64_t*, cudaStream_t);
+int64_t tc_act_m_pad(int64_t m);
 int group_epilogue_launch(const int32_t*, const double*, const double*, int64_t, int64_t, int64_t,
                           double*, uint16_t*, cudaStream_t);
 
@@ -183,8 +184,10 @@ int flexq_group_epilogue_f64(const int32_t* partials, const double* wscale,
   return group_epilogue_launch(partials, wscale, xscale, m, n, groups, y, y16, stream);
 }
 
+int64_t flexq_act_m_pad(int64_t m) { return m < 1 ? 0 : tc_act_m_pad(m); }
+
 int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size) {
-  const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
+  const int64_t m_pad = flexq_act_m_pad(m);
   T6Geom G(1, k, group_size);
   const int64_t frag = cdiv(flexq_act_frag_bytes(m_pad, k, group_size), 256) * 256;
   const int64_t vec = cdiv(G.ng * m_pad * 4, 256) * 256;
@@ -199,7 +202,7 @@ int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, 
     set_error("linear_forward: act_buf, flag and y are required");
     return FLEXQ_ERR_INVALID_INPUT;
   }
-  const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
+  const int64_t m_pad = flexq_act_m_pad(m);
   T6Geom G(1, k, group_size);
   char* base = reinterpret_cast<char*>(act_buf);
   const int64_t frag = cdiv(flexq_act_frag_bytes(m_pad, k, group_size), 256) * 256;

@@ -40,6 +40,7 @@ struct T6Params {
   int64_t m_total, tok0;        // trace / output token indexing
   int64_t ws_mstride;           // token stride of the split-K workspace
   int64_t ng, spg, ks, kb, rt;
+  int64_t act_mp8;              // token octets per k-block row of the activation operand
   T6Geom geo;
   int32_t* partials;
   void* y;
@@ -149,8 +150,8 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
 #pragma unroll
     for (int mt = 0; mt < MT; mt++) {
       if (mt * kTokTile + gq < p.m) {
-        const uint4* q = p.act + ((mt * p.kb + kb) * 2) * 32 + lane;
-        b[mt][0] = __ldg(q); b[mt][1] = __ldg(q + 32);
+        const uint4* q = p.act + (kb * p.act_mp8 + mt) * 64 + (2 * t) * 8 + gq;
+        b[mt][0] = __ldg(q); b[mt][1] = __ldg(q + 8);
       } else {
         b[mt][0] = make_uint4(0, 0, 0, 0); b[mt][1] = b[mt][0];
       }
@@ -176,9 +177,7 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
       unpack_t6(u4get(w0, jj), u4get(w1, jj), u4get(w2, jj), a);
 #pragma unroll
       for (int mt = 0; mt < MT; mt++) {
-        const uint4& bb = jj < 2 ? b[mt][0] : b[mt][1];
-        const uint32_t b0 = (jj & 1) ? bb.z : bb.x, b1 = (jj & 1) ? bb.w : bb.y;
-        mma_u8s8(P[mt], a, b0, b1);
+        mma_u8s8(P[mt], a, u4get(b[mt][0], jj), u4get(b[mt][1], jj));
       }
     }
     w0 = n0; w1 = n1; w2 = n2;
@@ -292,14 +291,36 @@ int gemv_stream_launch(const uint32_t*, const void*, int, const uint32_t*, const
                        const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
                        int, void*, cudaStream_t);
 
+int64_t tc_act_m_pad(int64_t m);
+bool gemm_tc_supported(int64_t m, int64_t m_pad, int64_t spg);
+int64_t gemm_tc_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
+int gemm_tc_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
+                   const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*, int,
+                   void*, cudaStream_t);
+
+// FLEXQ_DISABLE_TC=1 routes M > 16 to the mma.sync kernel (A/B runs)
+static bool tc_enabled() {
+  static int en = -1;
+  if (en < 0) {
+    const char* e = getenv("FLEXQ_DISABLE_TC");
+    en = (e && atoi(e) == 1) ? 0 : 1;
+  }
+  return en == 1;
+}
+
 int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int ksplit) {
   T6Geom G(n, k, gs);
   const int ks_eff = ksplit <= 0 ? auto_ksplit_t6(G.rt, G.kb) : ksplit;
   const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
-  int64_t bytes = ws_counters_offset(ks_eff, m_pad, G.rt) + cdiv(G.rt * 4, 256) * 256;
+  const int64_t mc = m_pad < kT6TokChunk ? m_pad : kT6TokChunk;
+  int64_t bytes = ws_counters_offset(ks_eff, mc, G.rt) + cdiv(G.rt * 4, 256) * 256;
   if (ksplit <= 0 && gemv_stream_supported(m, G.spg)) {
     const int64_t b2 = gemv_stream_workspace(m, n, k, gs);
     if (b2 > bytes) bytes = b2;
+  }
+  if (ksplit == 0 && gemm_tc_supported(m, tc_act_m_pad(m), G.spg)) {
+    const int64_t b3 = gemm_tc_workspace(m, n, k, gs);
+    if (b3 > bytes) bytes = b3;
   }
   return bytes;
 }
@@ -332,6 +353,10 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   if (ksplit <= 0 && gemv_stream_supported(m, G.spg) && (workspace || !fast))
     return gemv_stream_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
                               gs, partials, y, out_dtype, workspace, st);
+  // batched regime: tcgen05.mma kind::i8 with TMEM accumulators (gemm_tc.cu)
+  if (ksplit == 0 && tc_enabled() && gemm_tc_supported(m, m_pad, G.spg) && (workspace || !fast))
+    return gemm_tc_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k, gs,
+                          partials, y, out_dtype, workspace, st);
   if (ksplit <= 0) ksplit = auto_ksplit_t6(G.rt, G.kb);
   if (ksplit > 65535) ksplit = 65535;
   if (ksplit > 1 && fast && !workspace) {
@@ -344,7 +369,8 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
     p.geo = G;
     p.t6 = reinterpret_cast<const uint4*>(t6);
     p.wscale = wscale;
-    p.act = reinterpret_cast<const uint4*>(act_frag) + (m0 / kTokTile) * G.kb * 32 * 2;
+    p.act = reinterpret_cast<const uint4*>(act_frag) + (m0 / kTokTile) * 64;
+    p.act_mp8 = m_pad / kTokTile;
     p.xs = act_scale + m0;
     p.corr = act_corr + m0;
     p.m = mc;

@@ -139,10 +139,8 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
                      p.geo.scale_index(rg * kRowGroup, g_lo, 0) * SB,
                  wsb, &bar[s], pol_w);
     } else {
-#pragma unroll
-      for (int mt = 0; mt < MT; mt++)
-        bulk_g2s(dst + L::kOffB + mt * 1024, p.act + ((int64_t)mt * p.kb + kb) * 1024, 1024,
-                 &bar[s], pol_a);
+      bulk_g2s(dst + L::kOffB, p.act + (int64_t)kb * (p.m_pad >> 3) * 1024, MT * 1024, &bar[s],
+               pol_a);
       if (FAST) bulk_g2s(dst + L::kOffXs, p.xs + g_lo * p.m_pad, xsb, &bar[s], pol_a);
       bulk_g2s(dst + L::kOffCorr, p.corr + g_lo * p.m_pad, cb, &bar[s], pol_a);
     }
@@ -322,8 +320,8 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
     uint4 bv[MT][2], w[4][3];
 #pragma unroll
     for (int mt = 0; mt < MT; mt++) {
-      bv[mt][0] = lds128(st + L::kOffB + mt * 1024 + lane * 16);
-      bv[mt][1] = lds128(st + L::kOffB + mt * 1024 + 512 + lane * 16);
+      bv[mt][0] = lds128(st + L::kOffB + mt * 1024 + (2 * t) * 128 + gq * 16);
+      bv[mt][1] = lds128(st + L::kOffB + mt * 1024 + (2 * t + 1) * 128 + gq * 16);
     }
 #pragma unroll
     for (int r = 0; r < 4; r++)
@@ -352,11 +350,10 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
           unpack_t6(u4get(w[r][0], jj), u4get(w[r][1], jj), u4get(w[r][2], jj), a);
 #pragma unroll
           for (int mt = 0; mt < MT; mt++) {
-            const uint4& bb = bv[mt][jj >> 1];
             if (MODE == 0 && jj == 0)
-              mma_u8s8_zc(P[r][mt], a, bb.x, bb.y);
+              mma_u8s8_zc(P[r][mt], a, bv[mt][0].x, bv[mt][1].x);
             else
-              mma_u8s8(P[r][mt], a, (jj & 1) ? bb.z : bb.x, (jj & 1) ? bb.w : bb.y);
+              mma_u8s8(P[r][mt], a, u4get(bv[mt][0], jj), u4get(bv[mt][1], jj));
           }
         }
         bool gend;

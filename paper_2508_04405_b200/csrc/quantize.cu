@@ -65,15 +65,19 @@ __device__ __forceinline__ int quant_one(double v, double s, int bits) {
   return q < 0.0 ? -(int)a : (int)a;
 }
 
+// Byte of (token m, logical column c) in the activation operand:
+// [k-block][m_pad/8 token octets][8 k-cores][8 tokens][16 B] -- the K-major, no-swizzle
+// canonical UMMA layout.  Inside a k-block, padded slot s = 32*jj + 16*h + 4*t + b (k-step jj)
+// lives in k-core 2t+h at byte 4*jj+b, so lane (gq, t) of an mma.m16n8k32 finds its b0 / b1
+// registers of all four k-steps in the 16 B rows of k-cores 2t / 2t+1, and a tcgen05.mma of
+// K=32 over k-cores {2j, 2j+1} contracts the same slots as the converted weight tile.
 __device__ __forceinline__ int64_t frag_byte(const QuantArgs& A, int64_t m, int64_t c) {
   const int64_t g = c / A.gs, j = c - g * A.gs;
   const int64_t kp = g * A.spg * kKStep + j;
   const int64_t ks = kp >> 5, within = kp & 31;
   const int64_t kb = ks >> 2, jj = ks & 3;
-  const int64_t half = within >> 4, wi = within & 15;
-  const int64_t t = wi >> 2, byte = wi & 3;
-  const int64_t lane = (m & 7) * 4 + t, mt = m >> 3;
-  return T6Geom::act_word(A.kb, mt, kb, (int)jj, (int)half, (int)lane) * 4 + byte;
+  const int64_t h = within >> 4, t = (within & 15) >> 2, byte = within & 3;
+  return ((kb * (A.m_pad >> 3) + (m >> 3)) * 8 + 2 * t + h) * 128 + (m & 7) * 16 + jj * 4 + byte;
 }
 
 __device__ __forceinline__ void emit(const QuantArgs& A, int64_t r, int64_t c, int code) {

@@ -214,9 +214,9 @@ def t6_pack_activations(xcodes, xscales, k: int, group_size: int):
     t = _dev.torch()
     L = _lib.lib()
     m = xcodes.shape[0]
-    m_pad = -(-m // 8) * 8
+    m_pad = L.flexq_act_m_pad(m)
     ng = -(-k // group_size)
-    frag = t.empty(L.flexq_act_frag_bytes(m_pad, k, group_size) // 4, dtype=t.int32,
+    frag = t.zeros(L.flexq_act_frag_bytes(m_pad, k, group_size) // 4, dtype=t.int32,
                    device=xcodes.device)
     xs = t.zeros((ng, m_pad), dtype=t.float32, device=xcodes.device)
     corr = t.zeros((ng, m_pad), dtype=t.int32, device=xcodes.device)

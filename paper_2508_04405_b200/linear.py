@@ -94,7 +94,7 @@ class FlexQLinear:
         """(act_frag, xs, corr) pointers inside the act buffer (mirrors flexq_linear_forward)."""
         L = _lib.lib()
         act, _ = self.buffers(m)
-        m_pad = -(-m // 8) * 8
+        m_pad = L.flexq_act_m_pad(m)
         ng = -(-self.k // self.group_size)
         frag = -(-L.flexq_act_frag_bytes(m_pad, self.k, self.group_size) // 256) * 256
         vec = -(-(ng * m_pad * 4) // 256) * 256

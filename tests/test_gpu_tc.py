@@ -1,0 +1,114 @@
+"""GPU parity of the batched (M > 16) tcgen05.mma kind::i8 GEMM (csrc/gemm_tc.cu).
+
+Same bar as the decode kernels: INT32 group partials bit-exact against the CPU
+oracle's int_matmul_reference restatement (engine.py:337-365), fp16 y within
+max|y - y_ref| <= 1e-3 * max|y_ref| of the float64 oracle, identical partials to
+the mma.sync kernel, and run-to-run bit-identical outputs (the stream-K fixup
+combines split tiles in a fixed CTA order).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU hosts, skipped there
+    pytest.skip("needs a B200", allow_module_level=True)
+
+import paper_2508_04405_b200 as fq  # noqa: E402
+from oracle import c_oracle  # noqa: E402
+from paper_2508_04405_b200 import _lib  # noqa: E402
+from paper_2508_04405_b200.engine import t6_pack_activations, t6_pack_weights  # noqa: E402
+
+FP16_TOL = 1e-3
+AUTO, LEGACY = 0, -1  # ksplit: 0 = auto (tcgen05 for M > 16), -1 = the mma.sync kernel
+
+
+def max_rel(y, ref):
+    return float(np.max(np.abs(np.asarray(y, np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def case(m, n, k, q, gs, seed):
+    rng = np.random.default_rng(seed)
+    w = rng.standard_normal((n, k)).astype(np.float16)
+    x = rng.standard_normal((m, k)).astype(np.float16)
+    x[:, 5] *= 80  # outlier channel: full-range A8 codes
+    wc, wsc = c_oracle.quantize(w, 6, gs, True)
+    xc, xsc = c_oracle.quantize(x, q, gs, True)
+    y_ref, p_ref = c_oracle.int_matmul(wc, xc, wsc, xsc, gs, trace=True)
+    return w, x, (wc, wsc, xc, xsc), y_ref, p_ref
+
+
+def run(codes, m, n, k, gs, ksplit=AUTO, trace=True, fast=True):
+    wc, wsc, xc, xsc = codes
+    L = _lib.lib()
+    t6, wsp = t6_pack_weights(torch.from_numpy(wc).cuda(), torch.from_numpy(wsc).cuda(), k, gs, True)
+    frag, xs, corr, m_pad = t6_pack_activations(torch.from_numpy(xc).cuda(),
+                                                torch.from_numpy(xsc).cuda(), k, gs)
+    ng = -(-k // gs)
+    parts = torch.zeros((ng, m, n), dtype=torch.int32, device="cuda") if trace else None
+    y = torch.empty((m, n), dtype=torch.float16, device="cuda") if fast else None
+    ws = torch.zeros(L.flexq_gemm_workspace_bytes(m, n, k, gs, ksplit), dtype=torch.uint8,
+                     device="cuda")
+    _lib.check(L.flexq_gemm_t6(_lib.ptr(t6), _lib.ptr(wsp), 1, _lib.ptr(frag), _lib.ptr(xs),
+                               _lib.ptr(corr), m, m_pad, n, k, gs, _lib.ptr(parts), _lib.ptr(y),
+                               _lib.OUT_F16, _lib.ptr(ws), ksplit, _lib.stream()))
+    torch.cuda.synchronize()
+    return (y.float().cpu().numpy() if fast else None), (parts.cpu().numpy() if trace else None)
+
+
+def test_act_m_pad():
+    L = _lib.lib()
+    assert [L.flexq_act_m_pad(m) for m in (1, 8, 9, 16, 17, 32, 33, 64, 65, 128, 129, 256)] == \
+        [8, 8, 16, 16, 32, 32, 64, 64, 128, 128, 256, 256]
+
+
+@pytest.mark.parametrize("m,n,k,q,gs", [
+    (17, 128, 256, 6, 128),     # smallest tcgen05 batch, one tile
+    (32, 384, 1024, 8, 128),    # TN = 32
+    (48, 136, 1024, 6, 128),    # odd number of 64-row groups: half-empty last tile
+    (64, 1000, 2048, 8, 128),   # TN = 64, N not a multiple of 128
+    (65, 256, 1024, 6, 256),    # TN = 128, two k-blocks per group
+    (128, 512, 1536, 8, 384),   # three k-blocks per group
+    (129, 384, 1024, 6, 128),   # two token tiles
+    (200, 640, 2048, 8, 1024),  # long group: drained every 512 k, correction once per group
+    (256, 256, 2048, 6, 2048),  # per-channel (group = K)
+    (32, 128, 8192, 8, 128),    # one tile split across 64 CTAs: deep stream-K fixup
+])
+def test_tc_partials_and_fast_path(m, n, k, q, gs):
+    _, _, codes, y_ref, p_ref = case(m, n, k, q, gs, seed=m * 7 + n + gs)
+    y, parts = run(codes, m, n, k, gs)
+    assert np.array_equal(parts, p_ref)
+    assert max_rel(y, y_ref) <= FP16_TOL
+    y2, _ = run(codes, m, n, k, gs, trace=False)
+    assert np.array_equal(y, y2)  # trace on/off and run to run: identical fp16 output
+
+
+@pytest.mark.parametrize("m,n,k,q", [(64, 5120, 5120, 6), (256, 5120, 5120, 6), (96, 13824, 5120, 6),
+                                     (48, 5120, 13824, 8)])
+def test_tc_llama13b_shapes(m, n, k, q):
+    """LLaMA-2-13B linear shapes across the GEMV-to-GEMM crossover (BASELINE config 3)."""
+    _, _, codes, y_ref, p_ref = case(m, n, k, q, 128, seed=m + n)
+    y, parts = run(codes, m, n, k, 128)
+    assert np.array_equal(parts, p_ref)
+    assert max_rel(y, y_ref) <= FP16_TOL
+
+
+def test_tc_matches_mma_sync_kernel():
+    m, n, k, q, gs = 80, 768, 3072, 8, 128
+    _, _, codes, y_ref, p_ref = case(m, n, k, q, gs, seed=3)
+    y_tc, p_tc = run(codes, m, n, k, gs, AUTO)
+    y_ms, p_ms = run(codes, m, n, k, gs, LEGACY)
+    assert np.array_equal(p_tc, p_ref) and np.array_equal(p_ms, p_ref)
+    assert max_rel(y_tc, y_ref) <= FP16_TOL and max_rel(y_ms, y_ref) <= FP16_TOL
+
+
+@pytest.mark.parametrize("m", [24, 100, 256])
+def test_tc_public_api(m):
+    """FlexQLinear.__call__ at batched M: fused quantizer -> tcgen05 GEMM."""
+    n, k = 1536, 4096
+    w, x, _, y_ref, _ = case(m, n, k, 6, 128, seed=m)
+    lin = fq.FlexQLinear(w, activation_bits=6)
+    y = lin(torch.from_numpy(x).cuda()).float().cpu().numpy()
+    assert max_rel(y, y_ref) <= FP16_TOL
+    lin.check_errors()
