@@ -27,6 +27,10 @@ constexpr int kRowTile = 16;   // mma M (weight rows per A fragment)
 constexpr int kTokTile = 8;    // mma N (tokens per B fragment)
 constexpr int kRowGroup = 4;   // row tiles per T6 unit (64 weight rows share one B fragment)
 constexpr int kUnitBytes = kRowGroup * 3 * 512;  // T6 bytes per (row group, k-block) unit
+// act_corr holds kCorrBias + 32 * sum(codes) per (group, token): the fp32 bit pattern of
+// 12582912 + corr, which the tcgen05 epilogue subtracts from its seeded accumulator
+// directly (gemm_tc.cu); the integer kernels remove the bias.
+constexpr int32_t kCorrBias = 0x4B400000;
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -119,10 +123,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)  // suspend-time hint (ns): sleep in hardware, do not spin
       : "memory");
 }
 // 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
           int2 cr = make_int2(0, 0);
           if (first && mt * kTokTile < p.ws_mstride)
             cr = *reinterpret_cast<const int2*>(&p.corr[g * p.m_pad + mt * kTokTile + 2 * t]);
+          if (first) { cr.x -= kCorrBias; cr.y -= kCorrBias; }
           P[mt][0] = -cr.x; P[mt][1] = -cr.y; P[mt][2] = -cr.x; P[mt][3] = -cr.y;
         }
       }

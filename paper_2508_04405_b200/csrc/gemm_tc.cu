@@ -34,6 +34,8 @@
 // k-blocks); CTA c owns units [c*U/P, (c+1)*U/P), so every CTA streams the same number
 // of weight bytes for every shape.  A tile split across CTAs is combined in CTA order
 // by the last contributor (atomic counter) -- deterministic, as in gemv_stream.cu.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace flexq {
@@ -103,39 +105,56 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 
 // K-major, no-swizzle canonical layout: 8-row x 16 B core matrices, LBO = 128 B between
 // k-adjacent cores, SBO = 1024 B between 8-row groups (sm_100 descriptor version 1).
+// Used for the activation B tiles, which the quantizer writes in this layout.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
          ((uint64_t)(1024 >> 4) << 32) | (1ull << 46);
 }
+// K-major, 128 B swizzle: row r of the tile is 128 contiguous k-bytes at r * 128, its 16 B
+// chunk c stored at chunk c ^ (r & 7); SBO = 1024 B per 8-row atom.  The converters write
+// the A tile in this layout: a quarter-warp's eight 16 B stores then cover all 32 banks
+// (the no-swizzle layout puts four lanes of a quarter on the same banks).  The tile base
+// must be 1024 B aligned; a K=32 step advances the start address by 32 B.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
 
 constexpr int kTcRows = 128;                 // weight rows per tile (UMMA M)
 constexpr int kTcConvWarps = 4;              // warps 0-3
-constexpr int kTcWarpProdW = 4, kTcWarpMma = 5, kTcWarpProdA = 6, kTcWarpEpi0 = 7;
-constexpr int kTcEpiWarps = 8;               // warps 7-14
-constexpr int kTcThreads = (kTcWarpEpi0 + kTcEpiWarps) * 32;
+constexpr int kTcWarpProdW = 4, kTcWarpMma = 5, kTcWarpProdB = 6, kTcWarpProdS = 7;
+constexpr int kTcWarpEpi0 = 8;               // epilogue: warps 8 .. 8 + 4G - 1
 constexpr uint32_t kSeed = 0x4B400000u;      // fp32 bits of 12582912 = 1.5 * 2^23
 constexpr int kMaxDrainKb = 4;               // exact fp32 reinterpretation needs <= 512 k per drain
 
 template <int TN>
 struct TcCfg {
   static constexpr int SW = 6;                     // raw weight ring (12 KB stages)
-  static constexpr int SA = TN == 128 ? 3 : 4;     // A/B ring
-  static constexpr int NB = 2;                     // TMEM drain buffers
-  static constexpr int SS = 4;                     // column-table ring
+  static constexpr int SA = TN == 128 ? 3 : 4;     // converted A ring (16 KB stages)
+  static constexpr int SB = TN == 128 ? 4 : 8;     // activation B ring
+  // epilogue: G groups of 4 warps (one per TMEM lane quarter); group g drains the events
+  // d = g (mod G) into its own fp32 accumulator, so G events are in flight at once
+  static constexpr int G = TN == 64 ? 4 : 2;
+  static constexpr int kEpiWarps = 4 * G;
+  static constexpr int kThreads = (kTcWarpEpi0 + kEpiWarps) * 32;
+  static constexpr int NB = TN == 32 ? 8 : TN == 64 ? 4 : 2;  // TMEM drain buffers (multiple of G)
+  static constexpr int SS = 8;                     // scale/correction slot ring
   static constexpr int kRaw = 2 * kUnitBytes;
   static constexpr int kA = kTcRows * 128;
   static constexpr int kB = TN * 128;
-  static constexpr int kTab = TN * 12;             // negC[TN] f32, sx[TN] f32, corr[TN] i32
+  static constexpr int kTab = TN * 8 + 512;        // xs[TN] f32, corr[TN], ws of 2 row groups
   static constexpr int kOffRaw = 0;
-  static constexpr int kOffA = kOffRaw + SW * kRaw;
+  static constexpr int kOffA = kOffRaw + SW * kRaw;  // 1024 B aligned (128 B swizzle atoms)
+  static_assert(kOffA % 1024 == 0, "A tiles need 1024 B alignment");
   static constexpr int kOffB = kOffA + SA * kA;
-  static constexpr int kOffTab = kOffB + SA * kB;
-  static constexpr int kOffBar = kOffTab + SS * kTab;
-  static constexpr int kNumBars = 2 * SW + 3 * SA + 2 * NB + 2 * SS;
+  static constexpr int kOffTab = kOffB + SB * kB;
+  static constexpr int kOffConst = kOffTab + SS * kTab;  // TN x 12582912.f (the seed as fp32)
+  static constexpr int kOffBar = kOffConst + TN * 4;
+  static constexpr int kNumBars = 2 * SW + 2 * SA + 2 * SB + 2 * NB + 2 * SS;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
-  // NB drain buffers + the fp32 tile accumulator
-  static constexpr uint32_t kTmemCols = (NB + 1) * TN <= 64 ? 64 : (NB + 1) * TN <= 128 ? 128 : (NB + 1) * TN <= 256 ? 256 : 512;
-  static constexpr int CH = TN / 2;                // columns per epilogue thread
+  // NB drain buffers + G fp32 tile accumulators
+  static constexpr uint32_t kTmemCols = (NB + G) * TN <= 128 ? 128 : (NB + G) * TN <= 256 ? 256 : 512;
+  static_assert((NB + G) * TN <= 512 && NB % G == 0 && SS % G == 0, "TMEM / ring geometry");
   // instruction descriptor: D s32 (bits 4-5 = 2), A u8 (7-9 = 0), B s8 (10-12 = 1),
   // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
   static constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) |
@@ -160,7 +179,16 @@ struct TcParams {
   void* y;
   float* ws_part;
   unsigned* counters;
+  long long* trace_clk;  // debug timeline of CTA 0 (FLEXQ_TC_TIMELINE), normally NULL
+  int dbg;               // debug experiment bits (FLEXQ_TC_DBG), results invalid when set
 };
+
+// timeline record: [role][unit][event] clock64 stamps for CTA 0
+constexpr int kTlUnits = 64;
+__device__ __forceinline__ void tl_mark(const TcParams& p, int role, int64_t i, int ev) {
+  if (p.trace_clk && blockIdx.x == 0 && i < kTlUnits)
+    p.trace_clk[(role * kTlUnits + i) * 4 + ev] = clock64();
+}
 
 __device__ __forceinline__ int64_t tc_unit_start(int64_t c, int64_t units, int64_t P) {
   return c * units / P;
@@ -169,24 +197,106 @@ __device__ __forceinline__ int64_t tc_owner(int64_t u, int64_t units, int64_t P)
   return ((u + 1) * P - 1) / units;
 }
 
-// a drain event ends after k-block kb of a tile when the scale group ends, 4 k-blocks of
-// a long group have accumulated, the tile's K ends, or the CTA's range ends
-__device__ __forceinline__ bool tc_drain_end(int kb, int kbn, int kpg, bool range_end) {
-  const int kg = kb % kpg;
-  return range_end || kb == kbn - 1 || kg == kpg - 1 || (kg % kMaxDrainKb) == kMaxDrainKb - 1;
+// Walk of a CTA's unit range without per-unit divisions: unit = (tile, kb), tile =
+// (row tile rt, token tile tt); kg = kb within its scale group g.  A drain event ends
+// after a k-block when the group ends, 4 k-blocks of a long group have accumulated,
+// the tile's K ends, or the CTA's range ends.
+struct TcCursor {
+  int64_t u, u1;
+  int rt, tt, kb, g, kg;
+  __device__ TcCursor(const TcParams& p, int64_t u0, int64_t u1_) : u(u0), u1(u1_) {
+    const int64_t tile = u0 / p.kbn;
+    kb = (int)(u0 - tile * p.kbn);
+    rt = (int)(tile / p.tt);
+    tt = (int)(tile - (int64_t)rt * p.tt);
+    g = kb / p.kpg;
+    kg = kb - g * p.kpg;
+  }
+  __device__ bool valid() const { return u < u1; }
+  __device__ int64_t tile(const TcParams& p) const { return (int64_t)rt * p.tt + tt; }
+  __device__ bool tile_end(const TcParams& p) const { return kb == p.kbn - 1 || u == u1 - 1; }
+  __device__ bool drain_end(const TcParams& p) const {
+    return tile_end(p) || kg == p.kpg - 1 || (kg & (kMaxDrainKb - 1)) == kMaxDrainKb - 1;
+  }
+  __device__ void next(const TcParams& p) {
+    u++;
+    if (++kb == p.kbn) {
+      kb = 0; g = 0; kg = 0;
+      if (++tt == p.tt) { tt = 0; rt++; }
+    } else if (++kg == p.kpg) {
+      kg = 0; g++;
+    }
+  }
+};
+
+// packed fp32x2 math (FADD2 / FMUL2 / FFMA2 on sm_100)
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
+      "sub.rn.f32x2 rd, ra, rb;\nmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
+      "mul.rn.f32x2 rd, ra, rb;\nmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
+      "mov.b64 rc, {%6,%7};\nfma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// tcgen05.wait::ld with the loaded registers as operands, so no use can be scheduled above it
+__device__ __forceinline__ void tmem_wait_ld_r(uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                 "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]),
+                 "+r"(v[13]), "+r"(v[14]), "+r"(v[15])::"memory");
+}
+__device__ __forceinline__ void tmem_wait_ld_r2(uint32_t (&v)[16], uint32_t (&w)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+                 "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]),
+                 "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(w[0]), "+r"(w[1]), "+r"(w[2]),
+                 "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]), "+r"(w[8]), "+r"(w[9]),
+                 "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]), "+r"(w[14]), "+r"(w[15])::"memory");
+}
+__device__ __forceinline__ void tmem_ld16x(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
 }
 
 template <int TN, bool SF16, bool TRACE, bool FAST, int OUT>
-__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams p) {
+__global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParams p) {
   using C = TcCfg<TN>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* wfull = bars;
   uint64_t* wempty = wfull + C::SW;
   uint64_t* bfull = wempty + C::SW;
-  uint64_t* afull = bfull + C::SA;
-  uint64_t* abempty = afull + C::SA;
-  uint64_t* dfull = abempty + C::SA;
+  uint64_t* bempty = bfull + C::SB;
+  uint64_t* afull = bempty + C::SB;
+  uint64_t* aempty = afull + C::SA;
+  uint64_t* dfull = aempty + C::SA;
   uint64_t* dempty = dfull + C::NB;
   uint64_t* sfull = dempty + C::NB;
   uint64_t* sempty = sfull + C::SS;
@@ -196,15 +306,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t cta = blockIdx.x, P = p.nctas, U = p.units;
   const int64_t u0 = tc_unit_start(cta, U, P), u1 = tc_unit_start(cta + 1, U, P);
-  const int kbn = p.kbn, kpg = p.kpg;
+  const int kbn = p.kbn;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SW; i++) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], kTcConvWarps); }
-    for (int i = 0; i < C::SA; i++) {
-      mbar_init(&bfull[i], 1); mbar_init(&afull[i], kTcConvWarps); mbar_init(&abempty[i], 1);
-    }
-    for (int i = 0; i < C::NB; i++) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kTcEpiWarps); }
-    for (int i = 0; i < C::SS; i++) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kTcEpiWarps); }
+    for (int i = 0; i < C::SB; i++) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
+    for (int i = 0; i < C::SA; i++) { mbar_init(&afull[i], kTcConvWarps); mbar_init(&aempty[i], 1); }
+    for (int i = 0; i < C::NB; i++) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
+    for (int i = 0; i < C::SS; i++) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 4); }
     fence_mbar_init();
   }
   if (warp == kTcWarpMma) {
@@ -227,12 +336,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams p) {
     int wi = 0, ai = 0;
     uint32_t wph = 0, aph = 0;
     for (int64_t u = u0; u < u1; u++) {
+      if (warp == 0 && lane == 0) tl_mark(p, 0, u - u0, 0);
       mbar_wait(&wfull[wi], wph);
-      mbar_wait(&abempty[ai], aph ^ 1u);
+      if (warp == 0 && lane == 0) tl_mark(p, 0, u - u0, 1);
+      mbar_wait(&aempty[ai], aph ^ 1u);
+      if (warp == 0 && lane == 0) tl_mark(p, 0, u - u0, 2);
       const uint8_t* raw = smem + C::kOffRaw + wi * C::kRaw + rgl * kUnitBytes;
       uint8_t* A = smem + C::kOffA + ai * C::kA;
 #pragma unroll
       for (int rr = 0; rr < 2; rr++) {
+        if (p.dbg & 2) break;
         const int r = 2 * (warp & 1) + rr;
         const uint4 w0 = lds128(raw + (r * 3 + 0) * 512 + lane * 16);
         const uint4 w1 = lds128(raw + (r * 3 + 1) * 512 + lane * 16);
@@ -240,15 +353,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams p) {
         uint32_t a[4][4];  // [jj][reg]
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) unpack_t6(u4get(w0, jj), u4get(w1, jj), u4get(w2, jj), a[jj]);
-        const int r8 = 8 * rgl + 2 * r;  // 8-row group of rows 16r + gq (+8 -> r8 + 1)
-        sts128(A + ((r8 + 0) * 8 + 2 * t + 0) * 128 + gq * 16, a[0][0], a[1][0], a[2][0], a[3][0]);
-        sts128(A + ((r8 + 1) * 8 + 2 * t + 0) * 128 + gq * 16, a[0][1], a[1][1], a[2][1], a[3][1]);
-        sts128(A + ((r8 + 0) * 8 + 2 * t + 1) * 128 + gq * 16, a[0][2], a[1][2], a[2][2], a[3][2]);
-        sts128(A + ((r8 + 1) * 8 + 2 * t + 1) * 128 + gq * 16, a[0][3], a[1][3], a[2][3], a[3][3]);
+        // rows rho0 = 64 rgl + 16 r + gq and rho0 + 8 (both have rho & 7 == gq); logical
+        // chunk 2t+h of a row holds k-slots {32 jj + 16 h + 4 t + b}
+        uint8_t* row0 = A + (64 * rgl + 16 * r + gq) * 128;
+        uint8_t* row1 = row0 + 8 * 128;
+        sts128(row0 + (((2 * t + 0) ^ gq) << 4), a[0][0], a[1][0], a[2][0], a[3][0]);
+        sts128(row1 + (((2 * t + 0) ^ gq) << 4), a[0][1], a[1][1], a[2][1], a[3][1]);
+        sts128(row0 + (((2 * t + 1) ^ gq) << 4), a[0][2], a[1][2], a[2][2], a[3][2]);
+        sts128(row1 + (((2 * t + 1) ^ gq) << 4), a[0][3], a[1][3], a[2][3], a[3][3]);
       }
       fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
       __syncwarp();
       if (lane == 0) { mbar_arrive(&wempty[wi]); mbar_arrive(&afull[ai]); }
+      if (warp == 0 && lane == 0) tl_mark(p, 0, u - u0, 3);
       if (++wi == C::SW) { wi = 0; wph ^= 1u; }
       if (++ai == C::SA) { ai = 0; aph ^= 1u; }
     }
@@ -258,127 +375,131 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams p) {
       const uint64_t pol = l2_policy_evict_first();
       int wi = 0;
       uint32_t wph = 0;
-      for (int64_t u = u0; u < u1; u++) {
-        const int64_t tile = u / kbn;
-        const int kb = (int)(u - tile * kbn);
-        const int rg0 = (int)(tile / p.tt) * 2;
+      for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+        const int rg0 = c.rt * 2;
         const int nu = rg0 + 1 < p.rg ? 2 : 1;
         mbar_wait(&wempty[wi], wph ^ 1u);
         mbar_expect_tx(&wfull[wi], nu * kUnitBytes);
         uint8_t* dst = smem + C::kOffRaw + wi * C::kRaw;
-        bulk_g2s(dst, p.t6 + ((int64_t)rg0 * kbn + kb) * kUnitBytes, kUnitBytes, &wfull[wi], pol);
+        bulk_g2s(dst, p.t6 + ((int64_t)rg0 * kbn + c.kb) * kUnitBytes, kUnitBytes, &wfull[wi], pol);
         if (nu == 2)
-          bulk_g2s(dst + kUnitBytes, p.t6 + ((int64_t)(rg0 + 1) * kbn + kb) * kUnitBytes,
+          bulk_g2s(dst + kUnitBytes, p.t6 + ((int64_t)(rg0 + 1) * kbn + c.kb) * kUnitBytes,
                    kUnitBytes, &wfull[wi], pol);
         if (++wi == C::SW) { wi = 0; wph ^= 1u; }
       }
     }
-  } else if (warp == kTcWarpProdA) {
-    // ===== activation producer: B tiles + per-drain column tables =====
-    pdl_wait();
-    const uint64_t pol = l2_policy_evict_last();
-    int bi = 0, si = 0;
-    uint32_t bph = 0, sph = 0;
-    int ev_kb0 = -1;  // first k-block of the current drain event
-    for (int64_t u = u0; u < u1; u++) {
-      const int64_t tile = u / kbn;
-      const int kb = (int)(u - tile * kbn);
-      const int tt = (int)(tile % p.tt);
-      if (ev_kb0 < 0) ev_kb0 = kb;
-      if (lane == 0) {
-        mbar_wait(&abempty[bi], bph ^ 1u);
+  } else if (warp == kTcWarpProdB) {
+    // ===== activation producer: B tiles (L2-resident, SB deep ahead of the MMA) =====
+    if (lane == 0) {
+      pdl_wait();
+      const uint64_t pol = l2_policy_evict_last();
+      int bi = 0;
+      uint32_t bph = 0;
+      for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+        mbar_wait(&bempty[bi], bph ^ 1u);
         mbar_expect_tx(&bfull[bi], C::kB);
         bulk_g2s(smem + C::kOffB + bi * C::kB,
-                 p.act + ((int64_t)kb * (p.m_pad >> 3) + (int64_t)tt * (TN / 8)) * 1024, C::kB,
+                 p.act + ((int64_t)c.kb * (p.m_pad >> 3) + (int64_t)c.tt * (TN / 8)) * 1024, C::kB,
                  &bfull[bi], pol);
+        if (++bi == C::SB) { bi = 0; bph ^= 1u; }
       }
-      if (++bi == C::SA) { bi = 0; bph ^= 1u; }
-      if (tc_drain_end(kb, kbn, kpg, u == u1 - 1)) {
+    }
+  } else if (warp == kTcWarpProdS) {
+    // ===== slot producer: per drain event, xs / corr of the token tile and the weight
+    // scales of the 128 rows (SS events ahead of the epilogue) =====
+    if (lane == 0) {
+      pdl_wait();
+      const uint64_t pol = l2_policy_evict_last();
+      constexpr uint32_t swb = 4 * 8 * 2 * (SF16 ? 2 : 4);  // one row group's scales of a group
+      int si = 0;
+      uint32_t sph = 0;
+      for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+        if (!c.drain_end(p)) continue;
         mbar_wait(&sempty[si], sph ^ 1u);
-        const int g = kb / kpg;
-        const bool first = (ev_kb0 % kpg) == 0;  // this event holds the group's first k-block
-        float* negc = reinterpret_cast<float*>(smem + C::kOffTab + si * C::kTab);
-        float* sx = negc + TN;
-        int* cr = reinterpret_cast<int*>(sx + TN);
-        for (int col = lane; col < TN; col += 32) {
-          const int64_t idx = (int64_t)g * p.m_pad + (int64_t)tt * TN + col;
-          const int c = first ? __ldg(&p.corr[idx]) : 0;
-          negc[col] = -(12582912.0f + (float)c);
-          sx[col] = FAST ? __ldg(&p.xs[idx]) : 0.f;
-          cr[col] = c;
+        const int rg0 = c.rt * 2;
+        const int nrg = rg0 + 1 < p.rg ? 2 : 1;
+        uint8_t* slot = smem + C::kOffTab + si * C::kTab;
+        const int64_t col0 = (int64_t)c.g * p.m_pad + (int64_t)c.tt * TN;
+        mbar_expect_tx(&sfull[si], (FAST ? TN * 4 + nrg * swb : 0) + TN * 4);
+        bulk_g2s(slot + TN * 4, p.corr + col0, TN * 4, &sfull[si], pol);
+        if (FAST) {
+          bulk_g2s(slot, p.xs + col0, TN * 4, &sfull[si], pol);
+          for (int r = 0; r < nrg; r++)
+            bulk_g2s(slot + TN * 8 + r * swb,
+                     reinterpret_cast<const uint8_t*>(p.wscale) +
+                         p.geo.scale_index((int64_t)(rg0 + r) * kRowGroup, c.g, 0) * (swb / 32),
+                     swb, &sfull[si], pol);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sfull[si]);
         if (++si == C::SS) { si = 0; sph ^= 1u; }
-        ev_kb0 = -1;
       }
     }
   } else if (warp == kTcWarpMma) {
     // ===== MMA issuer =====
     if (lane == 0) {
-      int ai = 0, d = 0;
-      uint32_t aph = 0;
+      int ai = 0, bi = 0, b = 0;
+      uint32_t aph = 0, bph = 0, dph = 0;
       bool ev_open = false;
-      for (int64_t u = u0; u < u1; u++) {
-        const int64_t tile = u / kbn;
-        const int kb = (int)(u - tile * kbn);
-        const int b = d % C::NB;
+      for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+        tl_mark(p, 1, c.u - u0, 0);
         if (!ev_open) {
-          mbar_wait(&dempty[b], ((uint32_t)(d / C::NB) & 1u) ^ 1u);
+          mbar_wait(&dempty[b], dph ^ 1u);
           tc_fence_after();
           ev_open = true;
         }
-        mbar_wait(&bfull[ai], aph);
+        tl_mark(p, 1, c.u - u0, 1);
+        mbar_wait(&bfull[bi], bph);
+        tl_mark(p, 1, c.u - u0, 2);
         mbar_wait(&afull[ai], aph);
+        tl_mark(p, 1, c.u - u0, 3);
         tc_fence_after();
-        const uint64_t ad = umma_desc(smem_u32(smem + C::kOffA + ai * C::kA));
-        const uint64_t bd = umma_desc(smem_u32(smem + C::kOffB + ai * C::kB));
+        const uint64_t ad = umma_desc_sw128(smem_u32(smem + C::kOffA + ai * C::kA));
+        const uint64_t bd = umma_desc(smem_u32(smem + C::kOffB + bi * C::kB));
 #pragma unroll
-        for (int s = 0; s < 4; s++)  // k-cores {2s, 2s+1}: +256 B per K=32 step
-          tc_mma_i8(tmem + b * TN, ad + (uint64_t)(s * 16), bd + (uint64_t)(s * 16), C::kIdesc, 1u);
-        tc_commit(&abempty[ai]);
-        if (tc_drain_end(kb, kbn, kpg, u == u1 - 1)) {
+        for (int s = 0; s < 4; s++)  // K=32 step s: A +32 B (swizzled rows), B +256 B (2 cores)
+          tc_mma_i8(tmem + b * TN, ad + (uint64_t)(s * 2), bd + (uint64_t)(s * 16), C::kIdesc, 1u);
+        tc_commit(&aempty[ai]);
+        tc_commit(&bempty[bi]);
+        if (c.drain_end(p)) {
           tc_commit(&dfull[b]);
-          d++;
           ev_open = false;
+          if (++b == C::NB) { b = 0; dph ^= 1u; }
         }
         if (++ai == C::SA) { ai = 0; aph ^= 1u; }
+        if (++bi == C::SB) { bi = 0; bph ^= 1u; }
       }
     }
   } else if (warp >= kTcWarpEpi0) {
     // ===== epilogue =====
-    // The fp32 accumulator of the tile lives in TMEM too (columns [NB*TN, NB*TN + TN)),
-    // so the epilogue holds only 16 columns in registers at a time.
     const int e = warp - kTcWarpEpi0;
-    const int q = warp & 3;    // TMEM lane quarter this warp may access
-    const int hc = e >> 2;     // column half
-    constexpr int CH = C::CH;
-    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + hc * CH;
-    const uint32_t tacc = tl + C::NB * TN;
+    const int gi = e >> 2;       // event group
+    const int q = warp & 3;      // TMEM lane quarter this warp may access
+    constexpr int G = C::G, NT = C::kEpiWarps * 32;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);  // this thread's lane, column 0
+    const uint32_t tacc0 = tl + C::NB * TN;                  // accumulator of group 0
+    const uint32_t tacc = tacc0 + gi * TN;                   // this group's accumulator
     const int rho = 32 * q + lane;  // tile row of this thread
+    for (int b = gi; b < C::NB; b += G)
 #pragma unroll
-    for (int b = 0; b < C::NB; b++)
+      for (int c0 = 0; c0 < TN; c0 += 16) tmem_fill16(tl + b * TN + c0, kSeed);
 #pragma unroll
-      for (int c0 = 0; c0 < CH; c0 += 16) tmem_fill16(tl + b * TN + c0, kSeed);
+    for (int c0 = 0; c0 < TN; c0 += 16) tmem_fill16(tacc + c0, 0u);
     tmem_wait_st();
     tc_fence_before();
+    if (e == 0)
+      for (int i = lane; i < TN; i += 32) reinterpret_cast<float*>(smem + C::kOffConst)[i] = 12582912.f;
+    named_bar_sync(1, NT);
     pdl_wait();
 
-    // weight-scale index of this thread's row: T6 row group rg, row tile r, pair (gq, i)
+    // this thread's weight scale inside a slot: row group rgl, row tile r, pair (gq, half8)
     const int rgl = rho >> 6, r_in = (rho >> 4) & 3, gq = rho & 7, half8 = (rho >> 3) & 1;
-    auto load_sw = [&](int64_t tile, int g) -> float {
-      if constexpr (!FAST) return 0.f;
-      const int64_t rg = (tile / p.tt) * 2 + rgl;
-      if (rg >= p.rg) return 0.f;
-      const int64_t idx = p.geo.scale_index(rg * kRowGroup + r_in, g, gq) * 2 + half8;
-      if constexpr (SF16) return __half2float(reinterpret_cast<const __half*>(p.wscale)[idx]);
-      else return reinterpret_cast<const float*>(p.wscale)[idx];
-    };
+    const int sw_off = TN * 8 + rgl * (4 * 8 * 2 * (SF16 ? 2 : 4)) +
+                       (((r_in * 8) + gq) * 2 + half8) * (SF16 ? 2 : 4);
+    constexpr int FC = TN / G;  // flush columns per group
     auto store_row = [&](int64_t tt, int64_t n_row, int c0, const float (&a)[16]) {
       if (n_row >= p.n) return;
 #pragma unroll
       for (int j = 0; j < 16; j++) {
-        const int64_t m = tt * TN + hc * CH + c0 + j;
+        const int64_t m = tt * TN + c0 + j;
         if (m < p.m) {
           if constexpr (OUT == FLEXQ_OUT_F16)
             reinterpret_cast<__half*>(p.y)[m * p.n + n_row] = __float2half_rn(a[j]);
@@ -387,125 +508,181 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(TcParams p) {
         }
       }
     };
-
-    int d = 0, si = 0;
-    uint32_t sph = 0;
-    int ev_kb0 = -1;
-    bool acc_live = false;  // the TMEM accumulator holds this tile's earlier drains
-    for (int64_t u = u0; u < u1; u++) {
-      const int64_t tile = u / kbn;
-      const int kb = (int)(u - tile * kbn);
-      if (ev_kb0 < 0) ev_kb0 = kb;
-      const bool rend = u == u1 - 1;
-      if (!tc_drain_end(kb, kbn, kpg, rend)) continue;
-      const int g = kb / kpg;
-      const bool first = (ev_kb0 % kpg) == 0;
-      const float sw = load_sw(tile, g);
-      const int b = d % C::NB;
-      mbar_wait(&dfull[b], (uint32_t)(d / C::NB) & 1u);
-      mbar_wait(&sfull[si], sph);
-      tc_fence_after();
-      const float* tab = reinterpret_cast<const float*>(smem + C::kOffTab + si * C::kTab);
-      const float* negc = tab + hc * CH;
-      const float* sx = tab + TN + hc * CH;
-      const int* cr = reinterpret_cast<const int*>(tab + 2 * TN) + hc * CH;
-      const int64_t tt = tile % p.tt;
-      const int64_t n_row = (tile / p.tt) * kTcRows + rho;
-#pragma unroll 1
-      for (int c0 = 0; c0 < CH; c0 += 16) {
-        uint32_t v[32], av[32];
-        tmem_ld16(tl + b * TN + c0, v);
-        if (FAST && acc_live) tmem_ld16(tacc + c0, av);
-        tmem_wait_ld();
-        if constexpr (FAST) {
+    // sum of the G group accumulators over columns [c0, c0+16), which are zeroed
+    auto take_acc = [&](int c0, float (&a)[16]) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            const float4 nc = *reinterpret_cast<const float4*>(negc + c0 + j);
-            const float4 sv = *reinterpret_cast<const float4*>(sx + c0 + j);
-            const float n4[4] = {nc.x, nc.y, nc.z, nc.w}, s4[4] = {sv.x, sv.y, sv.z, sv.w};
+      for (int j = 0; j < 16; j++) a[j] = 0.f;
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-              const float prev = acc_live ? __uint_as_float(av[j + i]) : 0.f;
-              av[j + i] = __float_as_uint(fmaf(sw * s4[i], __uint_as_float(v[j + i]) + n4[i], prev));
-            }
-          }
-          asm volatile(
-              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
-              "%12,%13,%14,%15,%16};" ::"r"(tacc + c0),
-              "r"(av[0]), "r"(av[1]), "r"(av[2]), "r"(av[3]), "r"(av[4]), "r"(av[5]), "r"(av[6]),
-              "r"(av[7]), "r"(av[8]), "r"(av[9]), "r"(av[10]), "r"(av[11]), "r"(av[12]),
-              "r"(av[13]), "r"(av[14]), "r"(av[15])
-              : "memory");
-        }
-        if constexpr (TRACE) {
+      for (int g2 = 0; g2 < G; g2++) {
+        uint32_t av[16];
+        tmem_ld16x(tacc0 + g2 * TN + c0, av);
+        tmem_wait_ld_r(av);
 #pragma unroll
-          for (int j = 0; j < 16; j++) {
-            const int64_t m = tt * TN + hc * CH + c0 + j;
-            if (m < p.m && n_row < p.n) {
-              const int P = (int)(v[j] - kSeed) - (first ? cr[c0 + j] : 0);
-              atomicAdd(&p.partials[((int64_t)g * p.m + m) * p.n + n_row], P);
-            }
-          }
-        }
-        tmem_fill16(tl + b * TN + c0, kSeed);  // re-seed for the buffer's next group
+        for (int j = 0; j < 16; j++) a[j] += __uint_as_float(av[j]);
+        tmem_fill16(tacc0 + g2 * TN + c0, 0u);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) { mbar_arrive(&dempty[b]); mbar_arrive(&sempty[si]); }
-      d++;
-      if (++si == C::SS) { si = 0; sph ^= 1u; }
-      ev_kb0 = -1;
-      acc_live = true;
+    };
 
-      if (FAST && (kb == kbn - 1 || rend)) {
-        // ---- flush this tile: direct store, or the deterministic stream-K fixup ----
-        acc_live = false;
+    int d = 0;              // drain-event counter (all groups count every event)
+    int ev_kg0 = -1;        // kg of the event's first k-block
+    for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+      if (ev_kg0 < 0) ev_kg0 = c.kg;
+      if (!c.drain_end(p)) continue;
+      const bool first = ev_kg0 == 0;  // this event holds the group's first k-block
+      ev_kg0 = -1;
+      const int64_t tt = c.tt;
+      const int64_t n_row = (int64_t)c.rt * kTcRows + rho;
+      if (d % G == gi) {
+        const int b = d % C::NB, si = d % C::SS;
+        const uint32_t dph = (uint32_t)(d / C::NB) & 1u, sph = (uint32_t)(d / C::SS) & 1u;
+        if (e == 0 && lane == 0) tl_mark(p, 3, c.u - u0, 0);
+        mbar_wait(&dfull[b], dph);
+        if (e == 0 && lane == 0) tl_mark(p, 3, c.u - u0, 1);
+        mbar_wait(&sfull[si], sph);
+        if (e == 0 && lane == 0) tl_mark(p, 2, c.u - u0, 0);
+        tc_fence_after();
+        const uint8_t* slot = smem + C::kOffTab + si * C::kTab;
+        const float* sx = reinterpret_cast<const float*>(slot);
+        const int* cr = reinterpret_cast<const int*>(slot + TN * 4);
+        // column constant C = 12582912 (the seed) plus, in the event holding the group's first
+        // k-block, the offset-binary correction: corr slots carry kCorrBias + corr = the fp32
+        // bits of 12582912 + corr (exact for groups <= 512; longer groups convert explicitly)
+        const int cmode = !first ? 0 : (p.kpg <= kMaxDrainKb ? 1 : 2);
+        const float* cvp = cmode == 1 ? reinterpret_cast<const float*>(cr)
+                                      : reinterpret_cast<const float*>(smem + C::kOffConst);
+        if constexpr (FAST) {
+          float sw;
+          if constexpr (SF16) sw = __half2float(*reinterpret_cast<const __half*>(slot + sw_off));
+          else sw = *reinterpret_cast<const float*>(slot + sw_off);
+          const float2 sw2 = make_float2(sw, sw);
+#pragma unroll 1
+          for (int c0 = 0; c0 < TN; c0 += 16) {
+            // column table first (plain loads), then the TMEM round trip
+            float4 sv[4], cv[4];
+            if (p.dbg & 1) {
+#pragma unroll
+              for (int j = 0; j < 4; j++) { sv[j] = make_float4(sw, sw, sw, sw); cv[j] = sv[j]; }
+            } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              sv[j] = *reinterpret_cast<const float4*>(sx + c0 + 4 * j);
+              cv[j] = *reinterpret_cast<const float4*>(cvp + c0 + 4 * j);
+            }
+            }
+            if (cmode == 2) {
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const int4 c4 = *reinterpret_cast<const int4*>(cr + c0 + 4 * j);
+                cv[j] = make_float4(12582912.f + (float)(c4.x - kCorrBias), 12582912.f + (float)(c4.y - kCorrBias),
+                                    12582912.f + (float)(c4.z - kCorrBias), 12582912.f + (float)(c4.w - kCorrBias));
+              }
+            }
+            if (e == 0 && lane == 0 && c0 == 0) tl_mark(p, 2, c.u - u0, 1);
+            uint32_t v[16], av[16];
+            tmem_ld16x(tl + b * TN + c0, v);
+            tmem_ld16x(tacc + c0, av);
+            tmem_wait_ld_r2(v, av);
+            if (e == 0 && lane == 0 && c0 == 0) tl_mark(p, 2, c.u - u0, 2);
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              const float2 s01 = f2_mul(sw2, make_float2(sv[j].x, sv[j].y));
+              const float2 s23 = f2_mul(sw2, make_float2(sv[j].z, sv[j].w));
+              const float2 f01 = f2_sub(make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1])),
+                                        make_float2(cv[j].x, cv[j].y));
+              const float2 f23 = f2_sub(make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])),
+                                        make_float2(cv[j].z, cv[j].w));
+              const float2 a01 = f2_fma(s01, f01, make_float2(__uint_as_float(av[4 * j]), __uint_as_float(av[4 * j + 1])));
+              const float2 a23 = f2_fma(s23, f23, make_float2(__uint_as_float(av[4 * j + 2]), __uint_as_float(av[4 * j + 3])));
+              av[4 * j] = __float_as_uint(a01.x); av[4 * j + 1] = __float_as_uint(a01.y);
+              av[4 * j + 2] = __float_as_uint(a23.x); av[4 * j + 3] = __float_as_uint(a23.y);
+            }
+            tmem_st16(tacc + c0, av);
+            if constexpr (TRACE) {
+#pragma unroll
+              for (int j = 0; j < 16; j++) {
+                const int64_t m = tt * TN + c0 + j;
+                if (m < p.m && n_row < p.n) {
+                  const int P = (int)(v[j] - kSeed) - (first ? cr[c0 + j] - kCorrBias : 0);
+                  atomicAdd(&p.partials[((int64_t)c.g * p.m + m) * p.n + n_row], P);
+                }
+              }
+            }
+            tmem_fill16(tl + b * TN + c0, kSeed);  // re-seed for the buffer's next group
+            if (e == 0 && lane == 0 && c0 == 0) tl_mark(p, 2, c.u - u0, 3);
+          }
+        } else {  // trace only
+#pragma unroll 1
+          for (int c0 = 0; c0 < TN; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16x(tl + b * TN + c0, v);
+            tmem_wait_ld_r(v);
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+              const int64_t m = tt * TN + c0 + j;
+              if (m < p.m && n_row < p.n) {
+                const int P = (int)(v[j] - kSeed) - (first ? cr[c0 + j] - kCorrBias : 0);
+                atomicAdd(&p.partials[((int64_t)c.g * p.m + m) * p.n + n_row], P);
+              }
+            }
+            tmem_fill16(tl + b * TN + c0, kSeed);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(&dempty[b]); mbar_arrive(&sempty[si]); }
+        if (e == 0 && lane == 0) tl_mark(p, 3, c.u - u0, 2);
+      }
+      d++;
+
+      if (FAST && c.tile_end(p)) {
+        // ---- flush this tile: all groups' accumulators summed; direct store, or the
+        // deterministic stream-K fixup; accumulators are zeroed as they are read out ----
+        tc_fence_before();
+        named_bar_sync(1, NT);  // every group has drained its events of this tile
+        tc_fence_after();
+        const int64_t tile = c.tile(p);
         const int64_t first_c = tc_owner(tile * kbn, U, P);
         const int64_t last_c = tc_owner(tile * kbn + kbn - 1, U, P);
         if (first_c == last_c) {
 #pragma unroll 1
-          for (int c0 = 0; c0 < CH; c0 += 16) {
-            uint32_t av[32];
-            tmem_ld16(tacc + c0, av);
-            tmem_wait_ld();
+          for (int c0 = gi * FC; c0 < (gi + 1) * FC; c0 += 16) {
             float a[16];
-#pragma unroll
-            for (int j = 0; j < 16; j++) a[j] = __uint_as_float(av[j]);
+            take_acc(c0, a);
             store_row(tt, n_row, c0, a);
           }
+          tmem_wait_st();
           continue;
         }
         const int which = u0 >= tile * kbn ? 0 : 1;
-        float* slot = p.ws_part + ((cta * 2 + which) * TN + hc * CH) * (int64_t)kTcRows + rho;
+        float* wslot = p.ws_part + ((cta * 2 + which) * TN) * (int64_t)kTcRows + rho;
 #pragma unroll 1
-        for (int c0 = 0; c0 < CH; c0 += 16) {
-          uint32_t av[32];
-          tmem_ld16(tacc + c0, av);
-          tmem_wait_ld();
+        for (int c0 = gi * FC; c0 < (gi + 1) * FC; c0 += 16) {
+          float a[16];
+          take_acc(c0, a);
 #pragma unroll
-          for (int j = 0; j < 16; j++) slot[(c0 + j) * kTcRows] = __uint_as_float(av[j]);
+          for (int j = 0; j < 16; j++) wslot[(c0 + j) * kTcRows] = a[j];
         }
+        tmem_wait_st();
         __threadfence();
-        named_bar_sync(1, kTcEpiWarps * 32);
+        named_bar_sync(1, NT);
         if (e == 0 && lane == 0) {
           const unsigned prev = atom_add_acq_rel_gpu(&p.counters[tile], 1u);
           *flush_flag = prev == (unsigned)(last_c - first_c) ? 1 : 0;
         }
-        named_bar_sync(1, kTcEpiWarps * 32);
+        named_bar_sync(1, NT);
         const bool last = *flush_flag != 0;
-        named_bar_sync(1, kTcEpiWarps * 32);  // flag read by all before the next flush
+        named_bar_sync(1, NT);  // flag read by all before the next flush
         if (!last) continue;
         __threadfence();
 #pragma unroll 1
-        for (int c0 = 0; c0 < CH; c0 += 16) {
+        for (int c0 = gi * FC; c0 < (gi + 1) * FC; c0 += 16) {
           float a[16];
 #pragma unroll
           for (int j = 0; j < 16; j++) a[j] = 0.f;
-          for (int64_t c = first_c; c <= last_c; c++) {  // fixed CTA order: deterministic
-            const int wc = tc_unit_start(c, U, P) >= tile * kbn ? 0 : 1;
-            const float* src =
-                p.ws_part + ((c * 2 + wc) * TN + hc * CH + c0) * (int64_t)kTcRows + rho;
+          for (int64_t cc = first_c; cc <= last_c; cc++) {  // fixed CTA order: deterministic
+            const int wc = tc_unit_start(cc, U, P) >= tile * kbn ? 0 : 1;
+            const float* src = p.ws_part + ((cc * 2 + wc) * TN + c0) * (int64_t)kTcRows + rho;
 #pragma unroll
             for (int j = 0; j < 16; j++) a[j] += __ldcg(src + j * kTcRows);
           }
@@ -572,7 +749,7 @@ static int launch_tc_inst(const TcParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_status(e, "gemm_tc attribute");
     configured = true;
   }
-  cudaError_t e = launch_pdl(kern, dim3((unsigned)p.nctas), dim3(kTcThreads), (size_t)smem, st, p);
+  cudaError_t e = launch_pdl(kern, dim3((unsigned)p.nctas), dim3(TcCfg<TN>::kThreads), (size_t)smem, st, p);
   if (e != cudaSuccess) return cuda_status(e, "gemm_tc launch");
   return FLEXQ_OK;
 }
@@ -596,6 +773,16 @@ static int dispatch_tc(const TcParams& p, bool sf16, bool trace, bool fast, int 
 #undef FLEXQ_TC
   set_error("gemm_tc: unsupported flag combination");
   return FLEXQ_ERR_CONFIG;
+}
+
+// debug: copy CTA 0's last timeline to host (FLEXQ_TC_TIMELINE set); returns entries
+static long long* g_tl = nullptr;
+extern "C" int flexq_debug_tc_timeline(long long* host, int max_entries) {
+  const int n = 4 * kTlUnits * 4;
+  if (!g_tl || max_entries < n) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  return n;
 }
 
 int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const uint32_t* act_frag,
@@ -631,6 +818,12 @@ int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const 
   p.geo = G;
   p.partials = partials;
   p.y = y;
+  if (getenv("FLEXQ_TC_DBG")) p.dbg = atoi(getenv("FLEXQ_TC_DBG"));
+  if (getenv("FLEXQ_TC_TIMELINE")) {
+    if (!g_tl) cudaMalloc(&g_tl, 4 * kTlUnits * 4 * sizeof(long long));
+    cudaMemsetAsync(g_tl, 0, 4 * kTlUnits * 4 * sizeof(long long), st);
+    p.trace_clk = g_tl;
+  }
   if (workspace) {
     p.ws_part = reinterpret_cast<float*>(workspace);
     const int64_t sms = tc_sms() > 148 ? tc_sms() : 148;

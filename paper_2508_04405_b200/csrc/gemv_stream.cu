@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   auto init_groups = [&](const uint8_t* st, int64_t dg) {
 #pragma unroll
     for (int mt = 0; mt < MT; mt++) {
-      const int2 cr = reinterpret_cast<const int2*>(st + L::kOffCorr)[(dg * p.m_pad + mt * kTokTile) / 2 + t];
+      int2 cr = reinterpret_cast<const int2*>(st + L::kOffCorr)[(dg * p.m_pad + mt * kTokTile) / 2 + t];
+      cr.x -= kCorrBias; cr.y -= kCorrBias;
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         P[r][mt][0] = -cr.x; P[r][mt][1] = -cr.y; P[r][mt][2] = -cr.x; P[r][mt][3] = -cr.y;
@@ -330,7 +331,10 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
     if constexpr (MODE == 0) {
 #pragma unroll
       for (int mt = 0; mt < MT; mt++)
+      {
         corr0[mt] = reinterpret_cast<const int2*>(st + L::kOffCorr)[(mt * kTokTile) / 2 + t];
+        corr0[mt].x -= kCorrBias; corr0[mt].y -= kCorrBias;
+      }
     }
     if constexpr (MODE == 2) {
       if (grem == 0) init_groups(st, 0);  // this warp owns the group's first k-step

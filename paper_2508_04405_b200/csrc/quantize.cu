@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) quantize_warp_kernel(QuantArgs A) {
     for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
     if (lane == 0) {
       if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)s;
-      if (A.act_corr) A.act_corr[g * A.m_pad + r] = 32 * csum;
+      if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
     }
   }
 }
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(1024) quantize_cta_kernel(QuantArgs A) {
     for (int w = 0; w < nw; w++) tot += red_i[w];
     if (A.scales) A.scales[r * A.ng + g] = s;
     if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)s;
-    if (A.act_corr) A.act_corr[g * A.m_pad + r] = 32 * tot;
+    if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * tot;
   }
 }
 
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) codes_to_frag_kernel(QuantArgs A,
   for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
   if (lane == 0) {
     A.act_scale[g * A.m_pad + r] = (float)scales[r * A.ng + g];
-    A.act_corr[g * A.m_pad + r] = 32 * csum;
+    A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
   }
 }
 

@@ -1,0 +1,126 @@
+#!/usr/bin/env python
+"""M sweep of the W6Ax linear on one B200 (BASELINE configs 2-4: the GEMV-to-GEMM
+crossover on LLaMA-2 7B/13B/70B layer shapes).
+
+For every (layer shape, M) it times, with CUDA-graph replay and CUDA events:
+  gemm    the T6 GEMM alone on already-quantized activations (the kernel the roofline
+          is about: gemv_stream for M <= 16, gemm_tc (tcgen05) above),
+  fwd     the full online call FlexQLinear.forward (quantizer + GEMM, fp16 in/out),
+  mma     (M > 16) the same GEMM forced onto the mma.sync kernel (ksplit=-1), the
+          unpack-to-INT8 IMMA baseline the tcgen05 kernel replaces.
+Every timed graph cycles through enough distinct copies of the layer's packed
+weights (>= 2x the 126 MB L2) that each launch streams its weights from HBM.
+
+    python tools/sweep.py --model llama2-13b --ms 1,2,4,8,16,32,64,128,256 > out.jsonl
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 2**20
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="llama2-13b")
+    ap.add_argument("--ms", default="1,2,4,8,16,32,64,128,256")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--no-mma", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+
+    from paper_2508_04405_b200 import FlexQLinear, _lib
+    from paper_2508_04405_b200.shapes import MODELS, gemm_bytes, policy_kind, unfused
+
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    dev = torch.device("cuda", 0)
+    L = _lib.lib()
+    shapes = MODELS[args.model]
+    if args.model != "llama2-70b":
+        shapes = unfused(shapes)
+    ms = [int(v) for v in args.ms.split(",")]
+
+    def timed(fn, reps):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    for s in shapes:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(s.n + s.k)
+        w = torch.randn((s.n, s.k), generator=gen, device=dev, dtype=torch.float16)
+        base = FlexQLinear(w, 6, s.act_bits, 128, fp16_scales=True, layer_kind=policy_kind(s.name))
+        del w
+        copies = max(1, -(-2 * L2_BYTES // base.weight_bytes))
+        lays = [base]
+        for _ in range(copies - 1):  # distinct weight buffers, same values
+            c = object.__new__(FlexQLinear)
+            c.__dict__.update(base.__dict__)
+            c.t6, c.wscale, c._bufs = base.t6.clone(), base.wscale.clone(), {}
+            c.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            lays.append(c)
+        for m in ms:
+            x = torch.randn((m, s.k), device=dev, dtype=torch.float16)
+            outs = [torch.empty((m, s.n), dtype=torch.float16, device=dev) for _ in lays]
+            for lay, o in zip(lays, outs):
+                lay.forward(x, out=o)
+            torch.cuda.synchronize()
+
+            def fwd():
+                for lay, o in zip(lays, outs):
+                    lay.forward(x, out=o)
+
+            def gemm():
+                for lay, o in zip(lays, outs):
+                    lay.gemm_only(m, o)
+
+            t_fwd = timed(fwd, args.reps) / len(lays)
+            t_gemm = timed(gemm, args.reps) / len(lays)
+            row = {"model": args.model, "layer": s.name, "m": m, "n": s.n, "k": s.k,
+                   "q": s.act_bits, "kernel": "gemv_stream" if m <= 16 else "gemm_tc",
+                   "us_gemm": t_gemm * 1e3, "us_fwd": t_fwd * 1e3}
+            if m > 16 and not args.no_mma:
+                wsb = L.flexq_gemm_workspace_bytes(m, s.n, s.k, 128, -1)
+                wss = [torch.zeros(wsb, dtype=torch.uint8, device=dev) for _ in lays]
+
+                def mma():
+                    for lay, o, wsx in zip(lays, outs, wss):
+                        frag, xs, corr, m_pad = lay._act_views(m)
+                        _lib.check(L.flexq_gemm_t6(
+                            _lib.ptr(lay.t6), _lib.ptr(lay.wscale), 1, frag, xs, corr, m, m_pad,
+                            s.n, s.k, 128, None, _lib.ptr(o), _lib.OUT_F16, _lib.ptr(wsx), -1,
+                            _lib.stream()))
+
+                row["us_mma_sync"] = timed(mma, max(3, args.reps // 4)) / len(lays) * 1e3
+                del wss
+            b = gemm_bytes(m, s.n, s.k)
+            row["gbs_gemm"] = b / (t_gemm * 1e-3) / 1e9
+            row["frac_hbm"] = row["gbs_gemm"] / peak
+            row["tops_gemm"] = 2 * m * s.n * s.k / (t_gemm * 1e-3) / 1e12
+            row["tops_fwd"] = 2 * m * s.n * s.k / (t_fwd * 1e-3) / 1e12
+            if "us_mma_sync" in row:
+                row["tops_mma_sync"] = 2 * m * s.n * s.k / (row["us_mma_sync"] * 1e-6) / 1e12
+            print(json.dumps(row), flush=True)
+        del lays, base
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
