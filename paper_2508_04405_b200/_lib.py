@@ -12,7 +12,7 @@ import threading
 from .errors import ConfigError, DeviceError, FormatError, InvalidInputError, ShapeError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libflexq_sm100a.so")
+LIB_PATH = os.environ.get("FLEXQ_LIB") or os.path.join(_PKG, "_lib", "libflexq_sm100a.so")
 
 OK, ERR_INVALID, ERR_SHAPE, ERR_CONFIG, ERR_FORMAT, ERR_CUDA = 0, -1, -2, -3, -4, -5
 FLAG_NONFINITE, FLAG_NONPOS_SCALE = 1, 2

@@ -36,6 +36,10 @@
 // by the last contributor (atomic counter) -- deterministic, as in gemv_stream.cu.
 #include <type_traits>
 
+#ifndef FLEXQ_EXP
+#define FLEXQ_EXP 0  // experiment bits for A/B profiling builds only (results invalid if set)
+#endif
+
 #include "common.cuh"
 
 namespace flexq {
@@ -121,23 +125,30 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 }
 
 constexpr int kTcRows = 128;                 // weight rows per tile (UMMA M)
-constexpr int kTcConvWarps = 4;              // warps 0-3
+constexpr int kTcConvWarps = 4;              // warps 0-3: two 16-row tiles each per k-block
 constexpr int kTcWarpProdW = 4, kTcWarpMma = 5, kTcWarpProdB = 6, kTcWarpProdS = 7;
-constexpr int kTcWarpEpi0 = 8;               // epilogue: warps 8 .. 8 + 4G - 1
+constexpr int kTcWarpEpi0 = 8;               // epilogue: warps 8 .. 8 + kEpiWarps - 1
 constexpr uint32_t kSeed = 0x4B400000u;      // fp32 bits of 12582912 = 1.5 * 2^23
 constexpr int kMaxDrainKb = 4;               // exact fp32 reinterpretation needs <= 512 k per drain
 
 template <int TN>
 struct TcCfg {
   static constexpr int SW = 6;                     // raw weight ring (12 KB stages)
-  static constexpr int SA = TN == 128 ? 3 : 4;     // converted A ring (16 KB stages)
-  static constexpr int SB = TN == 128 ? 4 : 8;     // activation B ring
-  // epilogue: G groups of 4 warps (one per TMEM lane quarter); group g drains the events
-  // d = g (mod G) into its own fp32 accumulator, so G events are in flight at once
-  static constexpr int G = TN == 64 ? 4 : 2;
-  static constexpr int kEpiWarps = 4 * G;
+  static constexpr int SA = TN == 128 ? 4 : 5;     // operand ring: converted A + activation B
+  // Two epilogue designs, both 8 warps (two per TMEM lane quarter):
+  //  * kRegAcc (TN <= 64): each warp owns TN/2 columns of its 32 rows, the fp32 tile
+  //    accumulator lives in registers and a drained TMEM buffer is handed back to the MMA
+  //    warp as soon as it is in registers (NB = 8 buffers in flight);
+  //  * TN = 128: two event groups of 4 warps drain alternate events into their own fp32
+  //    accumulators in TMEM (the register file cannot hold 64 columns per thread here);
+  //    the MMA accumulates onto a seeded buffer (kSeed) that the epilogue re-seeds.
+  static constexpr bool kRegAcc = TN <= 64;
+  static constexpr int kEpiWarps = 8;
   static constexpr int kThreads = (kTcWarpEpi0 + kEpiWarps) * 32;
-  static constexpr int NB = TN == 32 ? 8 : TN == 64 ? 4 : 2;  // TMEM drain buffers (multiple of G)
+  static constexpr int CH = TN / 2;
+  static constexpr int G = kRegAcc ? 1 : 2;                // event groups (TMEM-acc design)
+  static constexpr int kDrainArrivals = kRegAcc ? 8 : 4;   // warps releasing one buffer
+  static constexpr int NB = kRegAcc ? 8 : 2;               // TMEM drain buffers
   static constexpr int SS = 8;                     // scale/correction slot ring
   static constexpr int kRaw = 2 * kUnitBytes;
   static constexpr int kA = kTcRows * 128;
@@ -147,14 +158,14 @@ struct TcCfg {
   static constexpr int kOffA = kOffRaw + SW * kRaw;  // 1024 B aligned (128 B swizzle atoms)
   static_assert(kOffA % 1024 == 0, "A tiles need 1024 B alignment");
   static constexpr int kOffB = kOffA + SA * kA;
-  static constexpr int kOffTab = kOffB + SB * kB;
+  static constexpr int kOffTab = kOffB + SA * kB;
   static constexpr int kOffConst = kOffTab + SS * kTab;  // TN x 12582912.f (the seed as fp32)
   static constexpr int kOffBar = kOffConst + TN * 4;
-  static constexpr int kNumBars = 2 * SW + 2 * SA + 2 * SB + 2 * NB + 2 * SS;
+  static constexpr int kNumBars = 2 * SW + 2 * SA + 2 * NB + 2 * SS;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
-  // NB drain buffers + G fp32 tile accumulators
-  static constexpr uint32_t kTmemCols = (NB + G) * TN <= 128 ? 128 : (NB + G) * TN <= 256 ? 256 : 512;
-  static_assert((NB + G) * TN <= 512 && NB % G == 0 && SS % G == 0, "TMEM / ring geometry");
+  static constexpr int kAccCols = kRegAcc ? 0 : G * TN;
+  static constexpr uint32_t kTmemCols = NB * TN + kAccCols <= 128 ? 128 : NB * TN + kAccCols <= 256 ? 256 : 512;
+  static_assert(NB * TN + kAccCols <= 512 && NB % G == 0 && SS % G == 0, "TMEM geometry");
   // instruction descriptor: D s32 (bits 4-5 = 2), A u8 (7-9 = 0), B s8 (10-12 = 1),
   // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
   static constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(TN >> 3) << 17) |
@@ -185,6 +196,15 @@ struct TcParams {
 
 // timeline record: [role][unit][event] clock64 stamps for CTA 0
 constexpr int kTlUnits = 64;
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// per-CTA wall marks (ns): [0] start, [1] MMA loop done, [2] epilogue done, [3] units
+__device__ __forceinline__ void cta_mark(const TcParams& p, int ev, long long v) {
+  if (p.trace_clk) p.trace_clk[4 * kTlUnits * 4 + blockIdx.x * 4 + ev] = v;
+}
 __device__ __forceinline__ void tl_mark(const TcParams& p, int role, int64_t i, int ev) {
   if (p.trace_clk && blockIdx.x == 0 && i < kTlUnits)
     p.trace_clk[(role * kTlUnits + i) * 4 + ev] = clock64();
@@ -292,10 +312,8 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* wfull = bars;
   uint64_t* wempty = wfull + C::SW;
-  uint64_t* bfull = wempty + C::SW;
-  uint64_t* bempty = bfull + C::SB;
-  uint64_t* afull = bempty + C::SB;
-  uint64_t* aempty = afull + C::SA;
+  uint64_t* afull = wempty + C::SW;   // A converted + B landed (4 converter warps + 1 TMA)
+  uint64_t* aempty = afull + C::SA;   // stage consumed by the MMAs (tcgen05.commit)
   uint64_t* dfull = aempty + C::SA;
   uint64_t* dempty = dfull + C::NB;
   uint64_t* sfull = dempty + C::NB;
@@ -310,10 +328,9 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SW; i++) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], kTcConvWarps); }
-    for (int i = 0; i < C::SB; i++) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
-    for (int i = 0; i < C::SA; i++) { mbar_init(&afull[i], kTcConvWarps); mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < C::NB; i++) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
-    for (int i = 0; i < C::SS; i++) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 4); }
+    for (int i = 0; i < C::SA; i++) { mbar_init(&afull[i], kTcConvWarps + 1); mbar_init(&aempty[i], 1); }
+    for (int i = 0; i < C::NB; i++) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], C::kDrainArrivals); }
+    for (int i = 0; i < C::SS; i++) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::kDrainArrivals); }
     fence_mbar_init();
   }
   if (warp == kTcWarpMma) {
@@ -328,11 +345,12 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   pdl_launch_dependents();
+  if (threadIdx.x == 0) { cta_mark(p, 0, gtimer()); cta_mark(p, 3, u1 - u0); }
 
   if (warp < kTcConvWarps) {
     // ===== converters: T6 unit -> u8 UMMA A tile =====
     const int gq = lane >> 2, t = lane & 3;
-    const int rgl = warp >> 1;
+    const int rgl = warp >> 1;  // 64-row group of this warp
     int wi = 0, ai = 0;
     uint32_t wph = 0, aph = 0;
     for (int64_t u = u0; u < u1; u++) {
@@ -345,8 +363,7 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       uint8_t* A = smem + C::kOffA + ai * C::kA;
 #pragma unroll
       for (int rr = 0; rr < 2; rr++) {
-        if (p.dbg & 2) break;
-        const int r = 2 * (warp & 1) + rr;
+        const int r = 2 * (warp & 1) + rr;  // 16-row tile
         const uint4 w0 = lds128(raw + (r * 3 + 0) * 512 + lane * 16);
         const uint4 w1 = lds128(raw + (r * 3 + 1) * 512 + lane * 16);
         const uint4 w2 = lds128(raw + (r * 3 + 2) * 512 + lane * 16);
@@ -396,12 +413,12 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       int bi = 0;
       uint32_t bph = 0;
       for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
-        mbar_wait(&bempty[bi], bph ^ 1u);
-        mbar_expect_tx(&bfull[bi], C::kB);
+        mbar_wait(&aempty[bi], bph ^ 1u);
+        mbar_expect_tx(&afull[bi], C::kB);
         bulk_g2s(smem + C::kOffB + bi * C::kB,
                  p.act + ((int64_t)c.kb * (p.m_pad >> 3) + (int64_t)c.tt * (TN / 8)) * 1024, C::kB,
-                 &bfull[bi], pol);
-        if (++bi == C::SB) { bi = 0; bph ^= 1u; }
+                 &afull[bi], pol);
+        if (++bi == C::SA) { bi = 0; bph ^= 1u; }
       }
     }
   } else if (warp == kTcWarpProdS) {
@@ -436,39 +453,194 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
   } else if (warp == kTcWarpMma) {
     // ===== MMA issuer =====
     if (lane == 0) {
-      int ai = 0, bi = 0, b = 0;
-      uint32_t aph = 0, bph = 0, dph = 0;
-      bool ev_open = false;
+      int ai = 0, b = 0;
+      uint32_t aph = 0, dph = 0;
+      bool ev_open = false, ev_first = true;
       for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
-        tl_mark(p, 1, c.u - u0, 0);
         if (!ev_open) {
           mbar_wait(&dempty[b], dph ^ 1u);
-          tc_fence_after();
           ev_open = true;
+          ev_first = true;
         }
-        tl_mark(p, 1, c.u - u0, 1);
-        mbar_wait(&bfull[bi], bph);
-        tl_mark(p, 1, c.u - u0, 2);
         mbar_wait(&afull[ai], aph);
-        tl_mark(p, 1, c.u - u0, 3);
         tc_fence_after();
         const uint64_t ad = umma_desc_sw128(smem_u32(smem + C::kOffA + ai * C::kA));
-        const uint64_t bd = umma_desc(smem_u32(smem + C::kOffB + bi * C::kB));
+        const uint64_t bd = umma_desc(smem_u32(smem + C::kOffB + ai * C::kB));
 #pragma unroll
         for (int s = 0; s < 4; s++)  // K=32 step s: A +32 B (swizzled rows), B +256 B (2 cores)
-          tc_mma_i8(tmem + b * TN, ad + (uint64_t)(s * 2), bd + (uint64_t)(s * 16), C::kIdesc, 1u);
+          tc_mma_i8(tmem + b * TN, ad + (uint64_t)(s * 2), bd + (uint64_t)(s * 16), C::kIdesc,
+                    (C::kRegAcc && ev_first && s == 0) ? 0u : 1u);
+        ev_first = false;
         tc_commit(&aempty[ai]);
-        tc_commit(&bempty[bi]);
         if (c.drain_end(p)) {
           tc_commit(&dfull[b]);
           ev_open = false;
           if (++b == C::NB) { b = 0; dph ^= 1u; }
         }
         if (++ai == C::SA) { ai = 0; aph ^= 1u; }
-        if (++bi == C::SB) { bi = 0; bph ^= 1u; }
       }
+      cta_mark(p, 1, gtimer());
     }
   } else if (warp >= kTcWarpEpi0) {
+    if constexpr (C::kRegAcc) {
+    // ===== epilogue =====
+    // Per drain event: tcgen05.ld the INT32 partial (TMEM -> registers), hand the buffer
+    // straight back to the MMA warp, then dequantise into the fp32 register accumulator:
+    //   acc += (sw * xs) * (as_float(P_u + 0x4B400000) - (12582912 + corr))
+    // where as_float(P_u + 0x4B400000) is exactly 12582912 + P_u for |P_u| < 2^22.
+    const int e = warp - kTcWarpEpi0;
+    const int q = warp & 3;    // TMEM lane quarter this warp may access
+    const int hc = e >> 2;     // column slice
+    constexpr int CH = C::CH;
+    constexpr int NT = C::kEpiWarps * 32;
+    constexpr int CW = 16;  // columns per TMEM round trip
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + hc * CH;
+    const int rho = 32 * q + lane;  // tile row of this thread
+    if (e == 0)
+      for (int i = lane; i < TN; i += 32) reinterpret_cast<float*>(smem + C::kOffConst)[i] = 12582912.f;
+    named_bar_sync(1, NT);
+    pdl_wait();
+
+    // this thread's weight scale inside a slot: row group rgl, row tile r, pair (gq, half8)
+    const int rgl = rho >> 6, r_in = (rho >> 4) & 3, gq = rho & 7, half8 = (rho >> 3) & 1;
+    const int sw_off = TN * 8 + rgl * (4 * 8 * 2 * (SF16 ? 2 : 4)) +
+                       (((r_in * 8) + gq) * 2 + half8) * (SF16 ? 2 : 4);
+    float acc[CH];
+#pragma unroll
+    for (int j = 0; j < CH; j++) acc[j] = 0.f;
+    auto store_row = [&](int64_t tt, int64_t n_row, const float (&a)[CH]) {
+      if (n_row >= p.n) return;
+#pragma unroll
+      for (int j = 0; j < CH; j++) {
+        const int64_t m = tt * TN + hc * CH + j;
+        if (m < p.m) {
+          if constexpr (OUT == FLEXQ_OUT_F16)
+            reinterpret_cast<__half*>(p.y)[m * p.n + n_row] = __float2half_rn(a[j]);
+          else
+            reinterpret_cast<float*>(p.y)[m * p.n + n_row] = a[j];
+        }
+      }
+    };
+
+    int b = 0, si = 0;
+    uint32_t dph = 0, sph = 0;
+    int ev_kg0 = -1;        // kg of the event's first k-block
+    for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+      if (ev_kg0 < 0) ev_kg0 = c.kg;
+      if (!c.drain_end(p)) continue;
+      const bool first = ev_kg0 == 0;  // this event holds the group's first k-block
+      ev_kg0 = -1;
+      const int64_t tt = c.tt;
+      const int64_t n_row = (int64_t)c.rt * kTcRows + rho;
+      mbar_wait(&dfull[b], dph);
+      tc_fence_after();
+      const uint8_t* slot = smem + C::kOffTab + si * C::kTab;
+      const float* sx = reinterpret_cast<const float*>(slot) + hc * CH;
+      const int* cr = reinterpret_cast<const int*>(slot + TN * 4) + hc * CH;
+      const int cmode = !first ? 0 : (p.kpg <= kMaxDrainKb ? 1 : 2);
+      const float* cvp = cmode == 1 ? reinterpret_cast<const float*>(cr)
+                                    : reinterpret_cast<const float*>(smem + C::kOffConst) + hc * CH;
+#pragma unroll
+      for (int w0 = 0; w0 < CH; w0 += CW) {
+        uint32_t v[CW];
+#pragma unroll
+        for (int h = 0; h < CW / 16; h++)
+          tmem_ld16x(tl + b * TN + w0 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&v[16 * h]));
+#pragma unroll
+        for (int h = 0; h < CW / 16; h++) tmem_wait_ld_r(*reinterpret_cast<uint32_t(*)[16]>(&v[16 * h]));
+        if (w0 + CW == CH) {  // the whole partial is in registers: release the TMEM buffer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[b]);
+        }
+        if (w0 == 0) mbar_wait(&sfull[si], sph);
+        if constexpr (FAST) {
+          float sw;
+          if constexpr (SF16) sw = __half2float(*reinterpret_cast<const __half*>(slot + sw_off));
+          else sw = *reinterpret_cast<const float*>(slot + sw_off);
+          const float2 sw2 = make_float2(sw, sw);
+#pragma unroll
+          for (int j = 0; j < CW; j += 4) {
+            const int col = w0 + j;
+            const float4 sv = *reinterpret_cast<const float4*>(sx + col);
+            float4 cv;
+            if (cmode == 2) {
+              const int4 c4 = *reinterpret_cast<const int4*>(cr + col);
+              cv = make_float4(12582912.f + (float)(c4.x - kCorrBias), 12582912.f + (float)(c4.y - kCorrBias),
+                               12582912.f + (float)(c4.z - kCorrBias), 12582912.f + (float)(c4.w - kCorrBias));
+            } else {
+              cv = *reinterpret_cast<const float4*>(cvp + col);
+            }
+            const float2 s01 = f2_mul(sw2, make_float2(sv.x, sv.y));
+            const float2 s23 = f2_mul(sw2, make_float2(sv.z, sv.w));
+            const float2 f01 = f2_sub(make_float2(__uint_as_float(v[j] + kSeed), __uint_as_float(v[j + 1] + kSeed)),
+                                      make_float2(cv.x, cv.y));
+            const float2 f23 = f2_sub(make_float2(__uint_as_float(v[j + 2] + kSeed), __uint_as_float(v[j + 3] + kSeed)),
+                                      make_float2(cv.z, cv.w));
+            const float2 a01 = f2_fma(s01, f01, make_float2(acc[col], acc[col + 1]));
+            const float2 a23 = f2_fma(s23, f23, make_float2(acc[col + 2], acc[col + 3]));
+            acc[col] = a01.x; acc[col + 1] = a01.y; acc[col + 2] = a23.x; acc[col + 3] = a23.y;
+          }
+        }
+        if constexpr (TRACE) {
+#pragma unroll
+          for (int j = 0; j < CW; j++) {
+            const int64_t m = tt * TN + hc * CH + w0 + j;
+            if (m < p.m && n_row < p.n) {
+              const int P = (int)v[j] - (first ? cr[w0 + j] - kCorrBias : 0);
+              atomicAdd(&p.partials[((int64_t)c.g * p.m + m) * p.n + n_row], P);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[si]);
+      if (++b == C::NB) { b = 0; dph ^= 1u; }
+      if (++si == C::SS) { si = 0; sph ^= 1u; }
+
+      if (FAST && c.tile_end(p)) {
+        // ---- flush this tile: direct store, or the deterministic stream-K fixup ----
+        const int64_t tile = c.tile(p);
+        const int64_t first_c = tc_owner(tile * kbn, U, P);
+        const int64_t last_c = tc_owner(tile * kbn + kbn - 1, U, P);
+        if (first_c != last_c) {
+          const int which = u0 >= tile * kbn ? 0 : 1;
+          float* wslot = p.ws_part + ((cta * 2 + which) * TN + hc * CH) * (int64_t)kTcRows + rho;
+#pragma unroll
+          for (int j = 0; j < CH; j++) wslot[j * kTcRows] = acc[j];
+          __threadfence();
+          named_bar_sync(1, NT);
+          if (e == 0 && lane == 0) {
+            const unsigned prev = atom_add_acq_rel_gpu(&p.counters[tile], 1u);
+            *flush_flag = prev == (unsigned)(last_c - first_c) ? 1 : 0;
+          }
+          named_bar_sync(1, NT);
+          const bool last = *flush_flag != 0;
+          named_bar_sync(1, NT);  // flag read by all before the next flush
+          if (last) {
+            __threadfence();
+#pragma unroll
+            for (int j = 0; j < CH; j++) acc[j] = 0.f;
+            for (int64_t cc = first_c; cc <= last_c; cc++) {  // fixed CTA order: deterministic
+              const int wc = tc_unit_start(cc, U, P) >= tile * kbn ? 0 : 1;
+              const float* src = p.ws_part + ((cc * 2 + wc) * TN + hc * CH) * (int64_t)kTcRows + rho;
+              float v[CH];
+#pragma unroll
+              for (int j = 0; j < CH; j++) v[j] = __ldcg(src + j * kTcRows);
+#pragma unroll
+              for (int j = 0; j < CH; j++) acc[j] += v[j];
+            }
+            store_row(tt, n_row, acc);
+            if (e == 0 && lane == 0) p.counters[tile] = 0u;
+          }
+        } else {
+          store_row(tt, n_row, acc);
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) acc[j] = 0.f;
+      }
+    }
+      } else {
     // ===== epilogue =====
     const int e = warp - kTcWarpEpi0;
     const int gi = e >> 2;       // event group
@@ -691,11 +863,13 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
         if (e == 0 && lane == 0) p.counters[tile] = 0u;
       }
     }
+      }
   }
 
   // ---- teardown: every role done with TMEM before the allocating warp frees it ----
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) cta_mark(p, 2, gtimer());
   if (warp == kTcWarpMma) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -778,7 +952,7 @@ static int dispatch_tc(const TcParams& p, bool sf16, bool trace, bool fast, int 
 // debug: copy CTA 0's last timeline to host (FLEXQ_TC_TIMELINE set); returns entries
 static long long* g_tl = nullptr;
 extern "C" int flexq_debug_tc_timeline(long long* host, int max_entries) {
-  const int n = 4 * kTlUnits * 4;
+  const int n = 4 * kTlUnits * 4 + 4 * 1024;
   if (!g_tl || max_entries < n) return 0;
   cudaDeviceSynchronize();
   cudaMemcpy(host, g_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -820,8 +994,8 @@ int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const 
   p.y = y;
   if (getenv("FLEXQ_TC_DBG")) p.dbg = atoi(getenv("FLEXQ_TC_DBG"));
   if (getenv("FLEXQ_TC_TIMELINE")) {
-    if (!g_tl) cudaMalloc(&g_tl, 4 * kTlUnits * 4 * sizeof(long long));
-    cudaMemsetAsync(g_tl, 0, 4 * kTlUnits * 4 * sizeof(long long), st);
+    if (!g_tl) cudaMalloc(&g_tl, (4 * kTlUnits * 4 + 4 * 1024) * sizeof(long long));
+    cudaMemsetAsync(g_tl, 0, (4 * kTlUnits * 4 + 4 * 1024) * sizeof(long long), st);
     p.trace_clk = g_tl;
   }
   if (workspace) {

@@ -23,11 +23,22 @@ def main():
         y = lay(x)
     torch.cuda.synchronize()
     L = _lib.lib()
-    buf = (ctypes.c_longlong * (4 * 64 * 4))()
+    nall = 4 * 64 * 4 + 4 * 1024
+    buf = (ctypes.c_longlong * nall)()
     fn = L.flexq_debug_tc_timeline
     fn.restype = ctypes.c_int
-    cnt = fn(buf, 4 * 64 * 4)
-    a = np.frombuffer(buf, dtype=np.int64).reshape(4, 64, 4)
+    cnt = fn(buf, nall)
+    allv = np.frombuffer(buf, dtype=np.int64)
+    a = allv[:4 * 64 * 4].reshape(4, 64, 4)
+    cm = allv[4 * 64 * 4:].reshape(1024, 4)
+    cm = cm[cm[:, 0] > 0]
+    t0g = cm[:, 0].min()
+    print(f"CTAs {len(cm)}: start spread {(cm[:,0].max()-t0g)/1e3:.2f} us; mma done "
+          f"min {(cm[:,1].min()-t0g)/1e3:.2f} max {(cm[:,1].max()-t0g)/1e3:.2f} us; end min "
+          f"{(cm[:,2].min()-t0g)/1e3:.2f} max {(cm[:,2].max()-t0g)/1e3:.2f} us; units {cm[:,3].min()}-{cm[:,3].max()}")
+    order = np.argsort(cm[:, 2])[-5:]
+    for i in order:
+        print(f"  slow cta: start {(cm[i,0]-t0g)/1e3:.2f} mma_done {(cm[i,1]-t0g)/1e3:.2f} end {(cm[i,2]-t0g)/1e3:.2f}")
     t0 = a[a > 0].min()
     names = ["conv(start,wfull,aempty,done)", "mma(start,dempty,bfull,afull)",
              "epi(sfull_ok,table_loaded,ld_done,chunk0_done)", "epi(start,dfull_ok,arrived)"]
