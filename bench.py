@@ -268,11 +268,13 @@ def main():
             traffic = prof["gemm_traffic_bytes_per_step"][key] / len(shapes)
     except Exception:
         pass
-    launches_per_fwd = 1 + -(-M // 64)
+    launches_per_fwd = 2  # fused activation quantizer + one GEMV/GEMM kernel per linear
     line = {
         "metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "int8 IMMA (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue, fp16 out",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": ("int8 IMMA mma.sync" if M <= 16 else "int8 tcgen05.mma kind::i8")
+                 + " (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue, fp16 out",
         "data": "synthetic: random-init INT6 weights of the real shapes (fp16 N(0,1) quantized), fp16 N(0,1) activations",
         "config": {"workload": f"{args.model} decoder-layer linears qkv,o,gate,up (W6A6) + down (W6A8), M={M}",
                    "batch": M, "group_size": 128, "scales": "fp16",
@@ -284,7 +286,9 @@ def main():
         "hbm_GBps_algorithmic": layer_b / (ms_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"flexq::gemv_t6_stream_kernel ({len(shapes)} launches/step, per-launch bytes in DESIGN.md sec. 4)",
+                     "kernel": ("flexq::gemv_t6_stream_kernel" if M <= 16 else
+                                "flexq::gemm_tc_kernel (tcgen05.mma kind::i8)")
+                               + f" ({len(shapes)} launches/step, per-launch bytes in DESIGN.md sec. 4)",
                      "peak_source": peak_kind, "gemm_us_per_step": ms_gemm * 1e3},
         "clocks": clk.summary(),
         "e2e": {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TOPS",

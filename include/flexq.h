@@ -158,6 +158,33 @@ int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, 
                          uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
                          cudaStream_t stream);
 
+/* ---- LLaMA-2 decode harness (BASELINE config 5) ---------
+ * Producers and glue around the W6Ax linears for an end-to-end decode step.  The
+ * reference has no model code; these are NOT part of its drop-in surface.
+ * The fused quantizers write the same activation operand as flexq_quantize (same m_pad
+ * rules, fp16 scales) from an fp16 intermediate h computed in the kernel:
+ *   rmsnorm:  h = weight * fp16(x * rsqrt(mean(x^2) + eps))    (LLaMA RMSNorm)
+ *   silu:     h = fp16(fp16(silu(g)) * u),  gate_up row = [g (cols) | u (cols)]
+ * and are bit-identical to flexq_quantize applied to that h (h_out may be NULL). */
+int flexq_rmsnorm_quantize(const void* x, int64_t x_stride, const void* weight, float eps,
+                           int64_t rows, int64_t cols, int bits, int64_t group_size,
+                           uint32_t* act_frag, float* act_scale, int32_t* act_corr, int64_t m_pad,
+                           uint32_t* flag, void* h_out, cudaStream_t stream);
+int flexq_silu_mul_quantize(const void* gate_up, int64_t x_stride, int64_t rows, int64_t cols,
+                            int bits, int64_t group_size, uint32_t* act_frag, float* act_scale,
+                            int32_t* act_corr, int64_t m_pad, uint32_t* flag, void* h_out,
+                            cudaStream_t stream);
+/* Rotate-half RoPE of q and k for each token's position pos[b] (device int32), k and v
+ * appended to the caches [batch, heads, max_len, head_dim] at pos[b]; q_out [batch, heads,
+ * head_dim].  qkv rows are [q | k | v] (heads * head_dim each). */
+int flexq_rope_kv_append(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache,
+                         void* q_out, int64_t batch, int heads, int head_dim, int64_t max_len,
+                         float theta, cudaStream_t stream);
+/* Single-query attention of q over cache positions [0, pos[b]] (head_dim 128). */
+int flexq_attn_decode(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
+                      void* out, int64_t batch, int heads, int head_dim, int64_t max_len,
+                      cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,11 @@ SIGNATURES = {
     "flexq_popcount_and": (i32, [vp, vp, i64, vp, vp]),
     "flexq_act_buf_bytes": (i64, [i64, i64, i64]),
     "flexq_linear_forward": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, vp, vp, vp, vp]),
+    "flexq_rmsnorm_quantize": (i32, [vp, i64, vp, ctypes.c_float, i64, i64, i32, i64, vp, vp, vp,
+                                     i64, vp, vp, vp]),
+    "flexq_silu_mul_quantize": (i32, [vp, i64, i64, i64, i32, i64, vp, vp, vp, i64, vp, vp, vp]),
+    "flexq_rope_kv_append": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, ctypes.c_float, vp]),
+    "flexq_attn_decode": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, vp]),
 }
 
 _lib = None

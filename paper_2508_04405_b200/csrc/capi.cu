@@ -40,6 +40,13 @@ int codes_to_frag_launch(const int8_t*, const double*, int64_t, int64_t, int64_t
                          uint32_t*, float*, int32_t*, cudaStream_t);
 int popcount_and_launch(const uint8_t*, const uint8_t*, int64_t, int64_t*, cudaStream_t);
 int64_t tc_act_m_pad(int64_t m);
+int fused_quant_launch(int, const void*, int64_t, const void*, float, int64_t, int64_t, int,
+                       int64_t, uint32_t*, float*, int32_t*, int64_t, uint32_t*, void*,
+                       cudaStream_t);
+int rope_kv_append_launch(const void*, const int*, void*, void*, void*, int64_t, int, int, int64_t,
+                          float, cudaStream_t);
+int attn_decode_launch(const void*, const void*, const void*, const int*, void*, int64_t, int, int,
+                       int64_t, cudaStream_t);
 int group_epilogue_launch(const int32_t*, const double*, const double*, int64_t, int64_t, int64_t,
                           double*, uint16_t*, cudaStream_t);
 
@@ -215,6 +222,36 @@ int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, 
   if (rc) return rc;
   return gemm_t6_launch(t6, wscale, scale_f16, act_frag, xs, corr, m, m_pad, n, k, group_size,
                         nullptr, y, FLEXQ_OUT_F16, workspace, 0, stream);
+}
+
+/* ---- LLaMA decode harness (BASELINE config 5) ---- */
+int flexq_rmsnorm_quantize(const void* x, int64_t x_stride, const void* weight, float eps,
+                           int64_t rows, int64_t cols, int bits, int64_t group_size,
+                           uint32_t* act_frag, float* act_scale, int32_t* act_corr, int64_t m_pad,
+                           uint32_t* flag, void* h_out, cudaStream_t stream) {
+  return fused_quant_launch(0, x, x_stride, weight, eps, rows, cols, bits, group_size, act_frag,
+                            act_scale, act_corr, m_pad, flag, h_out, stream);
+}
+
+int flexq_silu_mul_quantize(const void* gate_up, int64_t x_stride, int64_t rows, int64_t cols,
+                            int bits, int64_t group_size, uint32_t* act_frag, float* act_scale,
+                            int32_t* act_corr, int64_t m_pad, uint32_t* flag, void* h_out,
+                            cudaStream_t stream) {
+  return fused_quant_launch(1, gate_up, x_stride, nullptr, 0.f, rows, cols, bits, group_size,
+                            act_frag, act_scale, act_corr, m_pad, flag, h_out, stream);
+}
+
+int flexq_rope_kv_append(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache,
+                         void* q_out, int64_t batch, int heads, int head_dim, int64_t max_len,
+                         float theta, cudaStream_t stream) {
+  return rope_kv_append_launch(qkv, pos, k_cache, v_cache, q_out, batch, heads, head_dim, max_len,
+                               theta, stream);
+}
+
+int flexq_attn_decode(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
+                      void* out, int64_t batch, int heads, int head_dim, int64_t max_len,
+                      cudaStream_t stream) {
+  return attn_decode_launch(q, k_cache, v_cache, pos, out, batch, heads, head_dim, max_len, stream);
 }
 
 }  // extern "C"

@@ -276,22 +276,30 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
         for (int mt = 0; mt < MT; mt++)
 #pragma unroll
           for (int i = 0; i < 4; i++) acc[r][mt][i] = 0.f;
-      for (int64_t w = first; w <= last; w++) {  // fixed order; all loads of a slot in flight
-        const float* src = p.ws_part + (rg + w) * (int64_t)kSlot + lane;
-        float v[4][MT][4];
+      // fixed order; FB contributors' slots in flight per L2 round trip
+      constexpr int FB = ONE ? 4 : 2;
+      for (int64_t w = first; w <= last; w += FB) {
+        float v[FB][4][MT][4];
 #pragma unroll
-        for (int r = 0; r < 4; r++)
+        for (int f = 0; f < FB; f++) {
+          const float* src = p.ws_part + (rg + w + f) * (int64_t)kSlot + lane;
 #pragma unroll
-          for (int mt = 0; mt < MT; mt++)
+          for (int r = 0; r < 4; r++)
 #pragma unroll
-            for (int i = 0; i < 4; i++)
-              v[r][mt][i] = (ONE && (i & 1)) ? 0.f : __ldcg(src + ((r * MT + mt) * 4 + i) * 32);
+            for (int mt = 0; mt < MT; mt++)
 #pragma unroll
-        for (int r = 0; r < 4; r++)
+              for (int i = 0; i < 4; i++)
+                v[f][r][mt][i] = ((ONE && (i & 1)) || w + f > last)
+                                     ? 0.f : __ldcg(src + ((r * MT + mt) * 4 + i) * 32);
+        }
 #pragma unroll
-          for (int mt = 0; mt < MT; mt++)
+        for (int f = 0; f < FB; f++)
 #pragma unroll
-            for (int i = 0; i < 4; i++) acc[r][mt][i] += v[r][mt][i];
+          for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+              for (int i = 0; i < 4; i++) acc[r][mt][i] += v[f][r][mt][i];
       }
       if (lane == 0) p.counters[rg] = 0u;
     }
@@ -430,8 +438,9 @@ bool gemv_stream_supported(int64_t m, int64_t spg) { return m <= 16 && stream_mo
 static int stream_stages() {
   static int s = 0;
   if (!s) {
-    const char* e = getenv("FLEXQ_STREAM_STAGES");  // tuning knob for A/B runs
-    s = (e && atoi(e) == 3) ? 3 : 2;
+    const char* e = getenv("FLEXQ_STREAM_STAGES");  // tuning knob for A/B runs (2/3/4)
+    const int v = e ? atoi(e) : 0;
+    s = (v >= 2 && v <= 4) ? v : -1;  // -1: automatic
   }
   return s;
 }
@@ -453,7 +462,9 @@ static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 4) per_sm = 4;  // workspace slots are sized for <= 16 warps per SM
   int64_t warps = (int64_t)num_sms * per_sm * kSWarps;
-  const int64_t by_units = cdiv(p.units, kMinUnitsPerWarp);  // bounds the fixup fan-in
+  // bounds the fixup fan-in; deep rings (small layers) spread the units thinner so that a
+  // warp's whole range is in flight at once
+  const int64_t by_units = cdiv(p.units, S >= 4 ? 2 : kMinUnitsPerWarp);
   if (warps > by_units) warps = by_units;
   p.nw = warps;
   const unsigned ctas = (unsigned)cdiv(warps, kSWarps);
@@ -532,15 +543,20 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   }
   const bool trace = partials != nullptr, fast = y != nullptr;
   const bool sf16 = scale_f16 != 0;
-  const int S = stream_stages();
+  // small layers (fewer than ~6 units per warp at full occupancy): 4-stage rings
+  const int forced = stream_stages();
+  // ring depth by layer size (measured on B200, tools/sweep.py): small layers are latency-
+  // bound and want every unit of a warp in flight; large ones want more warps per SM
+  const int S = forced > 0 ? forced : (p.units <= 4096 ? 4 : p.units <= 12288 ? 3 : 2);
 #define FLEXQ_SM(MT_, MODE_, S_)                                                          \
   if (mt == MT_ && mode == MODE_ && S == S_)                                              \
     return dispatch_stream_flags<MT_, MODE_, S_>(p, sf16, trace, fast, out_dtype, sms, st);
   FLEXQ_SM(1, 0, 2) FLEXQ_SM(1, 1, 2) FLEXQ_SM(1, 2, 2)
   FLEXQ_SM(2, 0, 2) FLEXQ_SM(2, 1, 2) FLEXQ_SM(2, 2, 2)
   FLEXQ_SM(1, 0, 3) FLEXQ_SM(2, 0, 3)
+  FLEXQ_SM(1, 0, 4) FLEXQ_SM(2, 0, 4)
 #undef FLEXQ_SM
-  if (S == 3) {  // only MODE 0 has 3-stage instances; others use 2
+  if (S >= 3) {  // only MODE 0 has 3/4-stage instances; others use 2
 #define FLEXQ_SM2(MT_, MODE_)                                                             \
   if (mt == MT_ && mode == MODE_)                                                         \
     return dispatch_stream_flags<MT_, MODE_, 2>(p, sf16, trace, fast, out_dtype, sms, st);

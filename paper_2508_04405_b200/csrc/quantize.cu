@@ -330,3 +330,133 @@ int quantize_launch(const void* x, int dtype, int64_t rows, int64_t cols, int bi
 }
 
 }  // namespace flexq
+
+// ---- fused decode producers --------------------
+// RMSNorm -> quantize and SiLU(gate) * up -> quantize in one kernel: each warp builds the
+// fp16 intermediate h of one group in registers and quantizes it exactly as
+// quantize_warp_kernel does, so the codes, scales and corrections are bit-identical to
+// quantize(h) of that fp16 h.  h follows the LLaMA definitions:
+//   rmsnorm: h = w * fp16(x * rsqrt(mean(x^2) + eps))      (fp32 statistics)
+//   silu:    h = fp16(fp16(g / (1 + exp(-g))) * u)
+namespace flexq {
+struct FusedQuantArgs {
+  QuantArgs q;       // rows, cols, gs, ng, bits, fp16_scales, act_*, m_pad, flag, spg, kb
+  const __half* x;   // rmsnorm: [rows, x_stride]; silu: [rows, x_stride] = gate | up
+  const __half* w;   // rmsnorm weight [cols]
+  __half* h_out;     // optional fp16 h [rows, cols]
+  int64_t x_stride;
+  float eps;
+  int mode;          // 0 = rmsnorm, 1 = silu * up
+};
+
+// grid (rows, ceil(G / 8)), 8 warps: warp w quantizes group blockIdx.y * 8 + w of row
+// blockIdx.x.  RMSNorm: every CTA reduces the row's sum of squares itself (an L2-resident
+// re-read of one row), so the row is spread over G/8 CTAs instead of one.
+constexpr int kFusedWarps = 8;
+__device__ __forceinline__ __half fused_h(const FusedQuantArgs& F, const __half* xr, int64_t c,
+                                          float inv) {
+  if (F.mode == 0) return __hmul(F.w[c], __float2half_rn(__half2float(xr[c]) * inv));
+  const float g = __half2float(xr[c]);
+  return __hmul(__float2half_rn(g / (1.f + __expf(-g))), xr[F.q.cols + c]);
+}
+
+__global__ void __launch_bounds__(kFusedWarps * 32) fused_quant_kernel(FusedQuantArgs F) {
+  __shared__ float red[kFusedWarps];
+  pdl_wait();
+  pdl_launch_dependents();
+  const QuantArgs& A = F.q;
+  const int64_t r = blockIdx.x;
+  const int K = (int)A.cols;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const __half* xr = F.x + r * F.x_stride;
+  float inv = 0.f;
+  if (F.mode == 0) {
+    float ss = 0.f;
+    for (int i = tid * 8; i < K; i += kFusedWarps * 32 * 8) {
+      if (i + 8 <= K && (K & 7) == 0) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(xr + i);
+        const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const float2 f = __half22float2(h2[j]);
+          ss = fmaf(f.x, f.x, ss);
+          ss = fmaf(f.y, f.y, ss);
+        }
+      } else {
+        for (int j = i; j < i + 8 && j < K; j++) {
+          const float v = __half2float(xr[j]);
+          ss = fmaf(v, v, ss);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < kFusedWarps; w++) tot += red[w];  // same order in every CTA
+    inv = rsqrtf(tot / (float)K + F.eps);
+  }
+  const int64_t g = (int64_t)blockIdx.y * kFusedWarps + warp;
+  if (g >= A.ng) return;
+  const int64_t lo = g * A.gs, hi = min(lo + A.gs, A.cols);
+  double peak = 0.0;
+  bool finite = true;
+  for (int64_t c = lo + lane; c < hi; c += 32) {
+    const __half hv = fused_h(F, xr, c, inv);
+    if (F.h_out) F.h_out[r * K + c] = hv;
+    const double v = (double)__half2float(hv);
+    finite &= isfinite(v);
+    peak = fmax(peak, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+  if (!__all_sync(0xffffffffu, finite)) {
+    if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
+    peak = 0.0;
+  }
+  const double s = group_scale(peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
+  int csum = 0;
+  for (int64_t c = lo + lane; c < hi; c += 32) {
+    const double v = (double)__half2float(fused_h(F, xr, c, inv));
+    const int code = isfinite(v) ? quant_one(v, s, A.bits) : 0;
+    csum += code;
+    emit(A, r, c, code);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  if (lane == 0) {
+    if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)s;
+    if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
+  }
+}
+
+int fused_quant_launch(int mode, const void* x, int64_t x_stride, const void* w, float eps,
+                       int64_t rows, int64_t cols, int bits, int64_t gs, uint32_t* act_frag,
+                       float* act_scale, int32_t* act_corr, int64_t m_pad, uint32_t* flag,
+                       void* h_out, cudaStream_t st) {
+  if (rows < 1 || cols < 1 || bits < 2 || bits > 8 || gs < 1 || gs > 1024 || !flag || !act_frag ||
+      !act_scale || !act_corr || m_pad < rows || m_pad % kTokTile || (mode == 0 && !w)) {
+    set_error("fused quantize: bad arguments (rows=%lld cols=%lld bits=%d group=%lld m_pad=%lld)",
+              (long long)rows, (long long)cols, bits, (long long)gs, (long long)m_pad);
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  T6Geom geo(m_pad, cols, gs);
+  FusedQuantArgs F{};
+  F.q = QuantArgs{nullptr, rows, cols, gs, geo.ng, bits, 1, nullptr, nullptr,
+                  reinterpret_cast<uint8_t*>(act_frag), act_scale, act_corr, m_pad, flag, geo.spg,
+                  geo.kb};
+  F.x = reinterpret_cast<const __half*>(x);
+  F.w = reinterpret_cast<const __half*>(w);
+  F.h_out = reinterpret_cast<__half*>(h_out);
+  F.x_stride = x_stride;
+  F.eps = eps;
+  F.mode = mode;
+  cudaError_t e = launch_pdl(fused_quant_kernel,
+                             dim3((unsigned)rows, (unsigned)cdiv(geo.ng, kFusedWarps)),
+                             dim3(kFusedWarps * 32), 0, st, F);
+  if (e != cudaSuccess) return cuda_status(e, "fused quantize launch");
+  return FLEXQ_OK;
+}
+}  // namespace flexq

@@ -1,0 +1,180 @@
+"""GPU tests of the LLaMA decode harness (BASELINE config 5): the fused RMSNorm / SiLU*up
+quantizers are bit-identical to flexq quantize() of their own fp16 h and close to the torch
+formula; RoPE + KV append and decode attention match a torch fp32 reference; a small
+decoder's graph replay equals its eager steps and follows a torch reference built on the
+same FlexQLinear layers.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a B200", allow_module_level=True)
+
+import paper_2508_04405_b200 as fq  # noqa: E402
+from paper_2508_04405_b200 import _lib  # noqa: E402
+from paper_2508_04405_b200.llama import FlexQLlamaDecoder, LlamaConfig  # noqa: E402
+
+
+def _act_from_quantize(h, bits, lin):
+    """The act operand flexq_quantize writes for fp16 h (reference path of the fused ops)."""
+    L = _lib.lib()
+    m, k = h.shape
+    m_pad = L.flexq_act_m_pad(m)
+    frag = torch.zeros(L.flexq_act_frag_bytes(m_pad, k, 128) // 4, dtype=torch.int32, device="cuda")
+    ng = -(-k // 128)
+    xs = torch.zeros((ng, m_pad), dtype=torch.float32, device="cuda")
+    corr = torch.zeros((ng, m_pad), dtype=torch.int32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(L.flexq_quantize(_lib.ptr(h), _lib.DT_F16, m, k, bits, 128, 1, None, None,
+                                _lib.ptr(frag), _lib.ptr(xs), _lib.ptr(corr), m_pad, _lib.ptr(flag),
+                                _lib.stream()))
+    return frag, xs, corr, m_pad
+
+
+@pytest.mark.parametrize("mode,m,k,bits", [("rmsnorm", 1, 4096, 6), ("rmsnorm", 5, 5120, 8),
+                                           ("silu", 3, 11008, 8), ("silu", 8, 1408, 6)])
+def test_fused_quantizers_bit_exact(mode, m, k, bits):
+    L = _lib.lib()
+    g = torch.Generator(device="cuda").manual_seed(k + m)
+    x = torch.randn((m, 2 * k if mode == "silu" else k), generator=g, device="cuda").half()
+    w = (1 + 0.1 * torch.randn(k, generator=g, device="cuda")).half()
+    m_pad = L.flexq_act_m_pad(m)
+    frag = torch.zeros(L.flexq_act_frag_bytes(m_pad, k, 128) // 4, dtype=torch.int32, device="cuda")
+    ng = -(-k // 128)
+    xs = torch.zeros((ng, m_pad), dtype=torch.float32, device="cuda")
+    corr = torch.zeros((ng, m_pad), dtype=torch.int32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    h = torch.empty((m, k), dtype=torch.float16, device="cuda")
+    if mode == "rmsnorm":
+        rc = L.flexq_rmsnorm_quantize(_lib.ptr(x), x.stride(0), _lib.ptr(w), 1e-5, m, k, bits, 128,
+                                      _lib.ptr(frag), _lib.ptr(xs), _lib.ptr(corr), m_pad,
+                                      _lib.ptr(flag), _lib.ptr(h), _lib.stream())
+        xf = x.float()
+        h_ref = w * (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5)).half()
+    else:
+        rc = L.flexq_silu_mul_quantize(_lib.ptr(x), x.stride(0), m, k, bits, 128, _lib.ptr(frag),
+                                       _lib.ptr(xs), _lib.ptr(corr), m_pad, _lib.ptr(flag),
+                                       _lib.ptr(h), _lib.stream())
+        h_ref = torch.nn.functional.silu(x[:, :k].float()).half() * x[:, k:]
+    _lib.check(rc)
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 0
+    # same operand as the standalone quantizer applied to the kernel's own h (bit-exact)
+    frag2, xs2, corr2, _ = _act_from_quantize(h, bits, None)
+    assert torch.equal(frag, frag2) and torch.equal(xs[:, :m], xs2[:, :m])
+    assert torch.equal(corr[:, :m], corr2[:, :m])
+    # and h itself follows the LLaMA formula (fp16 rounding of fp32 statistics may differ by 1 ulp)
+    assert torch.allclose(h.float(), h_ref.float(), rtol=2e-3, atol=2e-3)
+
+
+def test_rope_and_attention_match_torch():
+    L = _lib.lib()
+    B, H, D, Lmax = 3, 4, 128, 40
+    g = torch.Generator(device="cuda").manual_seed(7)
+    kc = torch.zeros((B, H, Lmax, D), dtype=torch.float16, device="cuda")
+    vc = torch.zeros_like(kc)
+    q = torch.empty((B, H, D), dtype=torch.float16, device="cuda")
+    out = torch.empty((B, H * D), dtype=torch.float16, device="cuda")
+    hist = []
+    for step in range(12):
+        pos = torch.full((B,), step, dtype=torch.int32, device="cuda")
+        pos[1] = min(step, 5)  # ragged positions across the batch (overwrites slot 5)
+        qkv = torch.randn((B, 3 * H * D), generator=g, device="cuda").half()
+        _lib.check(L.flexq_rope_kv_append(_lib.ptr(qkv), _lib.ptr(pos), _lib.ptr(kc), _lib.ptr(vc),
+                                          _lib.ptr(q), B, H, D, Lmax, 10000.0, _lib.stream()))
+        _lib.check(L.flexq_attn_decode(_lib.ptr(q), _lib.ptr(kc), _lib.ptr(vc), _lib.ptr(pos),
+                                       _lib.ptr(out), B, H, D, Lmax, _lib.stream()))
+        hist.append((qkv.clone(), pos.clone()))
+    torch.cuda.synchronize()
+    # torch reference of the last step
+    inv = 10000.0 ** (-torch.arange(0, D // 2, device="cuda").float() * 2 / D)
+
+    def rot(x, p):
+        ang = p * inv
+        c, s = torch.cos(ang), torch.sin(ang)
+        a, b = x[..., :D // 2], x[..., D // 2:]
+        return torch.cat([a * c - b * s, b * c + a * s], -1)
+
+    Kr = torch.zeros((B, H, Lmax, D), device="cuda")
+    Vr = torch.zeros_like(Kr)
+    for qkv, pos in hist:
+        t3 = qkv.float().view(B, 3, H, D)
+        for b in range(B):
+            p = int(pos[b])
+            Kr[b, :, p] = rot(t3[b, 1], p)
+            Vr[b, :, p] = t3[b, 2]
+    qkv, pos = hist[-1]
+    t3 = qkv.float().view(B, 3, H, D)
+    for b in range(B):
+        p = int(pos[b])
+        qr = rot(t3[b, 0], p)  # [H, D]
+        assert torch.allclose(q[b].float(), qr, atol=2e-2, rtol=1e-2)
+        s = torch.einsum("hd,hld->hl", qr, Kr[b, :, :p + 1]) / D ** 0.5
+        o = torch.einsum("hl,hld->hd", torch.softmax(s, -1), Vr[b, :, :p + 1])
+        assert torch.allclose(out[b].float().view(H, D), o, atol=1e-2, rtol=1e-2)
+
+
+TINY = LlamaConfig(hidden=256, heads=2, ffn=512, layers=2, vocab=500)
+
+
+def _torch_reference_step(dec, x_tokens, kcache, vcache, pos):
+    """Torch decode step on the same FlexQLinear layers (their own quantize + GEMV)."""
+    cfg = dec.cfg
+    B, H, D = dec.batch, cfg.heads, cfg.head_dim
+    x = dec.embed[x_tokens]  # fp16 residual stream, as in the decoder
+    inv = cfg.rope_theta ** (-torch.arange(0, D // 2, device="cuda").float() * 2 / D)
+
+    def rms(v, w):
+        v = v.float()
+        return w * (v * torch.rsqrt(v.pow(2).mean(-1, keepdim=True) + cfg.eps)).half()
+
+    def rot(t, p):
+        ang = p * inv
+        c, s = torch.cos(ang), torch.sin(ang)
+        a, b = t[..., :D // 2], t[..., D // 2:]
+        return torch.cat([a * c - b * s, b * c + a * s], -1)
+
+    for li, lay in enumerate(dec.layers):
+        qkv = lay.qkv(rms(x, lay.norm1)).float().view(B, 3, H, D)
+        att = torch.empty((B, H, D), device="cuda")
+        for b in range(B):
+            qr = rot(qkv[b, 0], pos)
+            kcache[li][b, :, pos] = rot(qkv[b, 1], pos)
+            vcache[li][b, :, pos] = qkv[b, 2]
+            s = torch.einsum("hd,hld->hl", qr, kcache[li][b, :, :pos + 1]) / D ** 0.5
+            att[b] = torch.einsum("hl,hld->hd", torch.softmax(s, -1), vcache[li][b, :, :pos + 1])
+        x = x + lay.o(att.view(B, -1).half())
+        gu = lay.gate_up(rms(x, lay.norm2)).float()
+        hmid = (torch.nn.functional.silu(gu[:, :cfg.ffn]).half() * gu[:, cfg.ffn:].half())
+        x = x + lay.down(hmid)
+    return x.float()
+
+
+def test_tiny_decoder_graph_and_reference():
+    dec = FlexQLlamaDecoder(TINY, batch=3, max_len=16, seed=1)
+    dec.reset()
+    eager = []
+    for _ in range(6):
+        eager.append(dec.step().clone())
+    x_eager = dec.x.float().clone()
+    dec.reset()
+    dec.capture()
+    graph = [dec.step().clone() for _ in range(6)]
+    assert all(torch.equal(a, b) for a, b in zip(eager, graph))
+    assert torch.equal(dec.x.float(), x_eager)
+    dec.check_errors()
+    # one step against the torch reference on the same linears (fp32 glue)
+    dec2 = FlexQLlamaDecoder(TINY, batch=2, max_len=16, weights_from=dec)
+    dec2.reset(torch.tensor([3, 7], device="cuda"))
+    kc = [torch.zeros((2, TINY.heads, 16, TINY.head_dim), device="cuda") for _ in range(TINY.layers)]
+    vc = [torch.zeros_like(k) for k in kc]
+    for pos in range(3):
+        toks = dec2.tokens.clone()
+        x_ref = _torch_reference_step(dec2, toks, kc, vc, pos)
+        dec2.step()
+        err = (dec2.x.float() - x_ref).abs().max() / x_ref.abs().max()
+        assert err < 3e-2, f"step {pos}: rel err {err}"
+        dec2.tokens.copy_(toks + 1)  # same inputs for both paths next step
