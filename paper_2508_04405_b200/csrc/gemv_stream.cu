@@ -46,7 +46,14 @@ struct StreamParams {
   void* y;
   float* ws_part;
   unsigned* counters;
+  long long* tl;  // debug timeline (FLEXQ_GEMV_TIMELINE): per warp [start, pdl done, first data, loop done, end]
 };
+
+__device__ __forceinline__ long long gv_timer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Stage layout: [T6 weights 6 KB][B fragments MT x 1 KB][weight-scale slice][xs slice][corr slice]
 // A unit touches NGR groups at most: 4 when spg in {1,2} (MODE 1), otherwise 1.
@@ -92,6 +99,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   const int gq = lane >> 2, t = lane & 3;
   const int64_t gw = (int64_t)blockIdx.x * kSWarps + warp;
   if (gw >= p.nw) return;  // warp-uniform; no CTA-wide barriers below
+  if (p.tl && lane == 0) p.tl[gw * 5 + 0] = gv_timer();
   uint8_t* ring = smem + warp * (S * UB);
   uint64_t* bar = bars[warp];
   const int64_t u0 = gw * p.units / p.nw, u1 = (gw + 1) * p.units / p.nw;
@@ -171,6 +179,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   }
   pdl_wait();
   pdl_launch_dependents();
+  if (p.tl && lane == 0) p.tl[gw * 5 + 1] = gv_timer();
   if (lane == 0) {
     for (int s = 0; s < pro; s++) {
       issue(iu, irg, ikb, group_lo(ikb, ig), s, 1);
@@ -325,6 +334,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   for (int64_t u = u0; u < u1; u++) {
     const int g_lo = group_lo(kb, gdiv);
     mbar_wait(&bar[s], parity);
+    if (p.tl && lane == 0 && u == u0) p.tl[gw * 5 + 2] = gv_timer();
     const uint8_t* st = ring + s * UB;
     uint4 bv[MT][2], w[4][3];
 #pragma unroll
@@ -422,7 +432,9 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
       drain_groups(cur_rg, g, sw, sx);
     }
   }
+  if (p.tl && lane == 0) p.tl[gw * 5 + 3] = gv_timer();
   if (kb != 0) flush(cur_rg);  // (kb == 0: the last row group was already published)
+  if (p.tl && lane == 0) p.tl[gw * 5 + 4] = gv_timer();
 }
 
 // ---- host side ------------------------------------------------------------------------------
@@ -431,6 +443,15 @@ static int stream_mode(int64_t spg) {
   if (spg == 1 || spg == 2) return 1;
   if (spg % 4 == 0) return 2;
   return -1;
+}
+
+static long long* g_gemv_tl = nullptr;
+extern "C" int flexq_debug_gemv_timeline(long long* host, int max_entries) {
+  const int n = 148 * 16 * 5;
+  if (!g_gemv_tl || max_entries < n) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_gemv_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  return n;
 }
 
 bool gemv_stream_supported(int64_t m, int64_t spg) { return m <= 16 && stream_mode(spg) >= 0; }
@@ -534,6 +555,13 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   p.geo = G;
   p.partials = partials;
   p.y = y;
+  if (getenv("FLEXQ_GEMV_TIMELINE")) {
+    static long long* tlbuf = nullptr;
+    if (!tlbuf) cudaMalloc(&tlbuf, 148 * 16 * 5 * sizeof(long long));
+    cudaMemsetAsync(tlbuf, 0, 148 * 16 * 5 * sizeof(long long), st);
+    p.tl = tlbuf;
+    g_gemv_tl = tlbuf;
+  }
   const int mt = m <= 8 ? 1 : 2;
   if (workspace) {
     p.ws_part = reinterpret_cast<float*>(workspace);
