@@ -46,6 +46,7 @@ struct StreamParams {
   void* y;
   float* ws_part;
   unsigned* counters;
+  int rev;
   long long* tl;  // debug timeline (FLEXQ_GEMV_TIMELINE): per warp [start, pdl done, first data, loop done, end]
 };
 
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   if (p.tl && lane == 0) p.tl[gw * 5 + 0] = gv_timer();
   uint8_t* ring = smem + warp * (S * UB);
   uint64_t* bar = bars[warp];
-  const int64_t u0 = gw * p.units / p.nw, u1 = (gw + 1) * p.units / p.nw;
+  const int64_t gr = p.rev ? p.nw - 1 - gw : gw;  // debug: reversed range assignment
+  const int64_t u0 = gr * p.units / p.nw, u1 = (gr + 1) * p.units / p.nw;
 
   if (lane == 0) {
 #pragma unroll
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
     const int64_t last = unit_owner(rg * p.kb + p.kb - 1, p.nw, p.units);
     constexpr int kSlot = 4 * MT * 4 * 32;
     if (first != last) {
-      float* slot = p.ws_part + (rg + gw) * (int64_t)kSlot + lane;
+      float* slot = p.ws_part + (rg + gr) * (int64_t)kSlot + lane;
 #pragma unroll
       for (int r = 0; r < 4; r++)
 #pragma unroll
@@ -555,6 +557,7 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   p.geo = G;
   p.partials = partials;
   p.y = y;
+  if (getenv("FLEXQ_GEMV_REV")) p.rev = 1;
   if (getenv("FLEXQ_GEMV_TIMELINE")) {
     static long long* tlbuf = nullptr;
     if (!tlbuf) cudaMalloc(&tlbuf, 148 * 16 * 5 * sizeof(long long));

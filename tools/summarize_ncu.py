@@ -2,8 +2,9 @@
 
     python tools/summarize_ncu.py r01 [--model llama2-70b]
 
-Reads gpurun_out/<R>_gemv_m{1,8}.ncu-rep (--set full, one launch per layer of one
-step) and gpurun_out/<R>_launches_m1.csv (launch list), writes
+Reads gpurun_out/<R>_gemm_m{1,8,128}.ncu-rep (--set full, one launch per layer of one
+step: the GEMV for M <= 16, the tcgen05 GEMM above) and gpurun_out/<R>_launches_m1.csv
+(launch list), writes
 profiles/<R>_ncu.md (human summary) and updates profiles/ncu_summary.json
 (per-step DRAM traffic of the GEMM kernel, read by bench.py for roofline.traffic).
 """
@@ -68,12 +69,13 @@ def summarize(tag: str, model: str):
     summary_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
     summary.setdefault("gemm_traffic_bytes_per_step", {})
-    for m in (1, 8):
-        rep = os.path.join(ROOT, "gpurun_out", f"{tag}_gemv_m{m}.ncu-rep")
+    for m in (1, 8, 64, 128, 256):
+        rep = os.path.join(ROOT, "gpurun_out", f"{tag}_gemm_m{m}.ncu-rep")
         if not os.path.exists(rep):
             continue
         rows = raw_rows(rep)
-        lines += [f"## M={m}: `ncu --set full` on the {len(rows)} GEMV launches of one step", "",
+        kname = "gemv_t6_stream_kernel" if m <= 16 else "gemm_tc_kernel (tcgen05.mma kind::i8)"
+        lines += [f"## M={m}: `ncu --set full` on the {len(rows)} {kname} launches of one step", "",
                   "| layer | " + " | ".join(lbl for _, lbl in KEYS) + " |",
                   "|---" * (len(KEYS) + 1) + "|"]
         traffic = 0.0
