@@ -41,7 +41,10 @@ LLAMA2_13B = LlamaConfig(hidden=5120, heads=40, ffn=13824, layers=40, vocab=3200
 
 
 class _Layer:
-    def __init__(self, cfg: LlamaConfig, gen, dev, policy: BitPolicy, group_size: int):
+    KINDS = ("qkv_proj", "o_proj", "gate_proj", "down_proj")  # policy key of each linear
+
+    def __init__(self, cfg: LlamaConfig, gen, dev, policy: BitPolicy, group_size: int,
+                 keep_float: bool = False):
         t = _dev.torch()
         h, f = cfg.hidden, cfg.ffn
         std = h ** -0.5
@@ -51,15 +54,16 @@ class _Layer:
 
         self.norm1 = (1 + 0.05 * t.randn(h, generator=gen, device=dev)).half()
         self.norm2 = (1 + 0.05 * t.randn(h, generator=gen, device=dev)).half()
-        self.qkv = FlexQLinear(rnd(3 * h, h, std), 6, activation_bits("qkv_proj", policy),
-                               group_size, layer_kind="qkv_proj")
-        self.o = FlexQLinear(rnd(h, h, std), 6, activation_bits("o_proj", policy), group_size,
-                             layer_kind="o_proj")
-        # gate and up share their input: one GEMV over [gate; up]
-        self.gate_up = FlexQLinear(rnd(2 * f, h, std), 6, activation_bits("gate_proj", policy),
-                                   group_size, layer_kind="gate_proj")
-        self.down = FlexQLinear(rnd(h, f, f ** -0.5), 6, activation_bits("down_proj", policy),
-                                group_size, layer_kind="down_proj")
+        ws = [rnd(3 * h, h, std), rnd(h, h, std), rnd(2 * f, h, std), rnd(h, f, f ** -0.5)]
+        # gate and up share their input: one GEMV over [gate; up] (policy key gate_proj)
+        self.qkv, self.o, self.gate_up, self.down = (
+            FlexQLinear(w, 6, activation_bits(kind, policy), group_size, layer_kind=kind)
+            for w, kind in zip(ws, self.KINDS))
+        self.float_weights = ws if keep_float else None  # for sensitivity calibration
+
+    @property
+    def linears(self):
+        return (self.qkv, self.o, self.gate_up, self.down)
 
 
 class FlexQLlamaDecoder:
@@ -67,7 +71,8 @@ class FlexQLlamaDecoder:
 
     def __init__(self, cfg: LlamaConfig = LLAMA2_7B, batch: int = 1, max_len: int = 512,
                  policy: BitPolicy = DEFAULT_POLICY, group_size: int = 128, seed: int = 0,
-                 device="cuda", weights_from: "FlexQLlamaDecoder | None" = None):
+                 device="cuda", weights_from: "FlexQLlamaDecoder | None" = None,
+                 keep_float_layers: int = 1):
         t = _dev.torch()
         self.cfg, self.batch, self.max_len, self.group_size = cfg, batch, max_len, group_size
         dev = t.device(device)
@@ -82,7 +87,8 @@ class FlexQLlamaDecoder:
                                                                   src.lm_head)
         else:
             self.embed = (t.randn((cfg.vocab, h), generator=gen, device=dev) * 0.5).half()
-            self.layers = [_Layer(cfg, gen, dev, policy, group_size) for _ in range(cfg.layers)]
+            self.layers = [_Layer(cfg, gen, dev, policy, group_size, i < keep_float_layers)
+                           for i in range(cfg.layers)]
             self.norm_f = t.ones(h, dtype=t.float16, device=dev)
             self.lm_head = (t.randn((cfg.vocab, h), generator=gen, device=dev) * h ** -0.5).half()
         B = batch
@@ -110,27 +116,32 @@ class FlexQLlamaDecoder:
         return lin + self.lm_head.numel() * 2
 
     # -- one token for every sequence of the batch -------------------------------------------
-    def _fused_quant(self, kind: str, src, lin: FlexQLinear, cols: int, weight=None):
+    def _fused_quant(self, kind: str, src, lin: FlexQLinear, cols: int, weight=None, h_out=None):
         L = _lib.lib()
         frag, xs, corr, m_pad = lin._act_views(self.batch)
         if kind == "rmsnorm":
             rc = L.flexq_rmsnorm_quantize(_lib.ptr(src), src.stride(0), _lib.ptr(weight),
                                           self.cfg.eps, self.batch, cols, lin.activation_bits,
                                           self.group_size, frag, xs, corr, m_pad,
-                                          _lib.ptr(self.flag), None, _lib.stream())
+                                          _lib.ptr(self.flag), _lib.ptr(h_out), _lib.stream())
         else:
             rc = L.flexq_silu_mul_quantize(_lib.ptr(src), src.stride(0), self.batch, cols,
                                            lin.activation_bits, self.group_size, frag, xs, corr,
-                                           m_pad, _lib.ptr(self.flag), None, _lib.stream())
+                                           m_pad, _lib.ptr(self.flag), _lib.ptr(h_out),
+                                           _lib.stream())
         _lib.check(rc)
 
-    def _step(self):
+    def _step(self, record=None):
+        """One decode step; ``record`` (dict) collects the fp16 inputs of every linear of
+        the first len(record) layers (sensitivity calibration, eager mode only)."""
         t = _dev.torch()
         L = _lib.lib()
         cfg, B = self.cfg, self.batch
         t.index_select(self.embed, 0, self.tokens, out=self.x)
         for li, lay in enumerate(self.layers):
-            self._fused_quant("rmsnorm", self.x, lay.qkv, cfg.hidden, lay.norm1)
+            rec = record.get(li) if record is not None else None
+            h1 = t.empty_like(self.x) if rec is not None else None
+            self._fused_quant("rmsnorm", self.x, lay.qkv, cfg.hidden, lay.norm1, h1)
             lay.qkv.gemm_only(B, self.qkv_out)
             _lib.check(L.flexq_rope_kv_append(
                 _lib.ptr(self.qkv_out), _lib.ptr(self.pos), _lib.ptr(self.k_cache[li]),
@@ -142,16 +153,52 @@ class FlexQLlamaDecoder:
                 _lib.stream()))
             lay.o.forward(self.attn, out=self.o_out)
             self.x.add_(self.o_out)
-            self._fused_quant("rmsnorm", self.x, lay.gate_up, cfg.hidden, lay.norm2)
+            h2 = t.empty_like(self.x) if rec is not None else None
+            self._fused_quant("rmsnorm", self.x, lay.gate_up, cfg.hidden, lay.norm2, h2)
             lay.gate_up.gemm_only(B, self.gu)
-            self._fused_quant("silu", self.gu, lay.down, cfg.ffn)
+            h3 = t.empty((B, cfg.ffn), dtype=t.float16, device=self.device) if rec is not None else None
+            self._fused_quant("silu", self.gu, lay.down, cfg.ffn, None, h3)
             lay.down.gemm_only(B, self.d_out)
             self.x.add_(self.d_out)
+            if rec is not None:
+                for kind, h in zip(_Layer.KINDS, (h1, self.attn.clone(), h2, h3)):
+                    rec[kind].append(h)
         xf = self.x.float()
         hN = (xf * t.rsqrt(xf.pow(2).mean(-1, keepdim=True) + cfg.eps)).half() * self.norm_f
         logits = hN @ self.lm_head.t()
         t.argmax(logits, dim=-1, out=self.tokens)
         self.pos.add_(1)
+
+    def record_linear_inputs(self, steps: int = 4, layers: int = 1, max_rows: int = 256):
+        """LayerDumps (float weight, recorded fp16 inputs) of the first ``layers`` layers
+        over ``steps`` eager decode steps from the current state."""
+        from .sensitivity import LayerDump
+
+        record = {li: {k: [] for k in _Layer.KINDS} for li in range(layers)}
+        for _ in range(steps):
+            self._step(record)
+        dumps = []
+        for li in range(layers):
+            lay = self.layers[li]
+            if lay.float_weights is None:
+                raise ValueError(f"layer {li} kept no float weights (keep_float_layers)")
+            for kind, w in zip(_Layer.KINDS, lay.float_weights):
+                acts = _dev.torch().cat(record[li][kind])[:max_rows]
+                dumps.append(LayerDump(layer_name=f"model.layers.{li}.{kind}", layer_kind=kind,
+                                       weight=w.double().cpu().numpy(),
+                                       activations=acts.double().cpu().numpy()))
+        return dumps
+
+    def apply_policy(self, policy: BitPolicy) -> None:
+        """Set every linear's activation bits from ``policy`` (re-capture needed)."""
+        for lay in self.layers:
+            for lin, kind in zip(lay.linears, _Layer.KINDS):
+                lin.activation_bits = activation_bits(kind, policy)
+        self._graph = None
+
+    def policy_table(self) -> dict:
+        lay = self.layers[0]
+        return {kind: lin.activation_bits for lin, kind in zip(lay.linears, _Layer.KINDS)}
 
     def reset(self, tokens=None):
         t = _dev.torch()

@@ -17,9 +17,14 @@ python tools/decode_bench.py --model 7b --batches 1,2,4,8 --steps 128 --warmup 3
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"gemv|quantize|gemm" -c 40 --csv --log-file gpurun_out/${R}_launches_m1.csv \
     python bench.py --steps 3 --warmup 1 --e2e-steps 1 --no-cpu-baseline > /dev/null 2>&1
-# full sections for the 5 GEMM launches of one step
+# full sections for the 5 GEMM launches of one step; exported to CSV on the box (the
+# reports themselves would exceed gpurun's 64 MiB copy-back), one small report kept
 for m in 1 8 128; do
-  ncu --set full --import-source on --clock-control none -k regex:"gemv|gemm_tc" -c 5 -o gpurun_out/${R}_gemm_m$m \
+  ncu --set full --import-source on --clock-control none -k regex:"gemv|gemm_tc" -c 5 -o /tmp/${R}_gemm_m$m \
       python bench.py --batch $m --steps 3 --warmup 1 --e2e-steps 1 --no-cpu-baseline > /dev/null 2>&1
+  ncu -i /tmp/${R}_gemm_m$m.ncu-rep --page raw --csv > gpurun_out/${R}_gemm_m${m}_raw.csv
+  ncu -i /tmp/${R}_gemm_m$m.ncu-rep --page details --csv > gpurun_out/${R}_gemm_m${m}_details.csv
 done
-ls -la gpurun_out
+ncu --set full --import-source on --clock-control none -k regex:"gemv" -c 1 -o gpurun_out/${R}_gemv_m1_one \
+    python bench.py --steps 3 --warmup 1 --e2e-steps 1 --no-cpu-baseline > /dev/null 2>&1
+du -sh gpurun_out; ls -la gpurun_out

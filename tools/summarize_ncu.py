@@ -40,8 +40,12 @@ _SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def raw_rows(rep: str):
-    """Rows of `ncu --page raw`, with byte metrics converted to bytes."""
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Rows of `ncu --page raw` (from a report, or its exported _raw.csv), bytes in bytes."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -70,7 +74,9 @@ def summarize(tag: str, model: str):
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
     summary.setdefault("gemm_traffic_bytes_per_step", {})
     for m in (1, 8, 64, 128, 256):
-        rep = os.path.join(ROOT, "gpurun_out", f"{tag}_gemm_m{m}.ncu-rep")
+        rep = os.path.join(ROOT, "gpurun_out", f"{tag}_gemm_m{m}_raw.csv")
+        if not os.path.exists(rep):
+            rep = os.path.join(ROOT, "gpurun_out", f"{tag}_gemm_m{m}.ncu-rep")
         if not os.path.exists(rep):
             continue
         rows = raw_rows(rep)
