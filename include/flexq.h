@@ -129,6 +129,15 @@ int flexq_gemm_t6(const uint32_t* t6, const void* wscale, int scale_f16,
                   int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
                   cudaStream_t stream);
 
+/* Same, with an optional fused residual (y and residual of out_dtype, [m, n]; residual
+ * may alias y): y = acc + residual, one rounding.  Used by the decode step to fold the
+ * transformer's residual add into the linear's epilogue. */
+int flexq_gemm_t6_ex(const uint32_t* t6, const void* wscale, int scale_f16,
+                     const uint32_t* act_frag, const float* act_scale, const int32_t* act_corr,
+                     int64_t m, int64_t m_pad, int64_t n, int64_t k, int64_t group_size,
+                     int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
+                     const void* residual, cudaStream_t stream);
+
 /* BTC-equivalent bit-serial path: AND + popcount over FLXQ-P planes.
  * Replaces group_matmul_fused(wp, xp, ...)  (engine.py:290-334): wwords /
  * xwords from flexq_pack_planes with their chunk_m (reference defaults: 8 for
@@ -157,6 +166,11 @@ int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, 
                          const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
                          uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
                          cudaStream_t stream);
+/* Same with a fused fp16 residual [m, n] (may alias y): y = x W^T + residual. */
+int flexq_linear_forward_ex(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
+                            const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
+                            uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
+                            const void* residual, cudaStream_t stream);
 
 /* ---- LLaMA-2 decode harness (BASELINE config 5) ---------
  * Producers and glue around the W6Ax linears for an end-to-end decode step.  The

@@ -40,11 +40,15 @@ SIGNATURES = {
     "flexq_pack_act_t6": (i32, [vp, vp, i64, i64, i64, i64, vp, vp, vp, vp]),
     "flexq_gemm_workspace_bytes": (i64, [i64, i64, i64, i64, i32]),
     "flexq_gemm_t6": (i32, [vp, vp, i32, vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, i32, vp, i32, vp]),
+    "flexq_gemm_t6_ex": (i32, [vp, vp, i32, vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, i32, vp, i32,
+                               vp, vp]),
     "flexq_gemm_bitserial": (i32, [vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, i32, i32, vp, vp, i32, vp, i32, vp]),
     "flexq_group_epilogue_f64": (i32, [vp, vp, vp, i64, i64, i64, vp, vp, vp]),
     "flexq_popcount_and": (i32, [vp, vp, i64, vp, vp]),
     "flexq_act_buf_bytes": (i64, [i64, i64, i64]),
     "flexq_linear_forward": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, vp, vp, vp, vp]),
+    "flexq_linear_forward_ex": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, vp, vp, vp, vp,
+                                      vp]),
     "flexq_rmsnorm_quantize": (i32, [vp, i64, vp, ctypes.c_float, i64, i64, i32, i64, vp, vp, vp,
                                      i64, vp, vp, vp]),
     "flexq_silu_mul_quantize": (i32, [vp, i64, i64, i64, i32, i64, vp, vp, vp, i64, vp, vp, vp]),

@@ -31,7 +31,7 @@ int pack_t6_launch(const int8_t*, const double*, int64_t, int64_t, int64_t, int,
 int64_t gemm_t6_workspace(int64_t, int64_t, int64_t, int64_t, int);
 int gemm_t6_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
                    const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
-                   int, void*, int, cudaStream_t);
+                   int, void*, int, const void*, cudaStream_t);
 int64_t gemm_bitserial_workspace(int64_t, int64_t, int64_t, int);
 int gemm_bitserial_launch(const uint8_t*, const uint8_t*, const float*, const float*, int64_t,
                           int64_t, int64_t, int, int, int64_t, int, int, int32_t*, void*, int,
@@ -172,7 +172,16 @@ int flexq_gemm_t6(const uint32_t* t6, const void* wscale, int scale_f16,
                   int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
                   cudaStream_t stream) {
   return gemm_t6_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
-                        group_size, partials, y, out_dtype, workspace, ksplit, stream);
+                        group_size, partials, y, out_dtype, workspace, ksplit, nullptr, stream);
+}
+
+int flexq_gemm_t6_ex(const uint32_t* t6, const void* wscale, int scale_f16,
+                     const uint32_t* act_frag, const float* act_scale, const int32_t* act_corr,
+                     int64_t m, int64_t m_pad, int64_t n, int64_t k, int64_t group_size,
+                     int32_t* partials, void* y, int out_dtype, void* workspace, int ksplit,
+                     const void* residual, cudaStream_t stream) {
+  return gemm_t6_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
+                        group_size, partials, y, out_dtype, workspace, ksplit, residual, stream);
 }
 
 int flexq_gemm_bitserial(const uint8_t* wwords, const uint8_t* xwords, const float* wscale,
@@ -201,10 +210,10 @@ int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size) {
   return frag + 2 * vec;
 }
 
-int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
-                         const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
-                         uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
-                         cudaStream_t stream) {
+static int linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
+                          const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
+                          uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
+                          const void* residual, cudaStream_t stream) {
   if (!act_buf || !flag || !y) {
     set_error("linear_forward: act_buf, flag and y are required");
     return FLEXQ_ERR_INVALID_INPUT;
@@ -221,7 +230,23 @@ int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, 
                            act_frag, xs, corr, m_pad, flag, stream);
   if (rc) return rc;
   return gemm_t6_launch(t6, wscale, scale_f16, act_frag, xs, corr, m, m_pad, n, k, group_size,
-                        nullptr, y, FLEXQ_OUT_F16, workspace, 0, stream);
+                        nullptr, y, FLEXQ_OUT_F16, workspace, 0, residual, stream);
+}
+
+int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
+                         const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
+                         uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
+                         cudaStream_t stream) {
+  return linear_forward(t6, wscale, scale_f16, xbits, x, m, n, k, group_size, y, act_buf,
+                        workspace, flag, nullptr, stream);
+}
+
+int flexq_linear_forward_ex(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
+                            const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
+                            uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
+                            const void* residual, cudaStream_t stream) {
+  return linear_forward(t6, wscale, scale_f16, xbits, x, m, n, k, group_size, y, act_buf,
+                        workspace, flag, residual, stream);
 }
 
 /* ---- LLaMA decode harness (BASELINE config 5) ---- */

@@ -196,6 +196,14 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v
   return old;
 }
 
+// optional fused residual of the output store: y[i] = acc + res[i] (res may alias y)
+template <int OUT>
+__device__ __forceinline__ float residual_at(const void* res, int64_t i) {
+  if (!res) return 0.f;
+  if constexpr (OUT == FLEXQ_OUT_F16) return __half2float(reinterpret_cast<const __half*>(res)[i]);
+  else return reinterpret_cast<const float*>(res)[i];
+}
+
 __device__ __forceinline__ uint32_t u4get(const uint4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }

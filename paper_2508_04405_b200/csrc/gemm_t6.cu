@@ -46,6 +46,7 @@ struct T6Params {
   void* y;
   float* ws_part;
   unsigned* counters;
+  const void* res;  // optional residual added at the store
   int ksplit;
 };
 
@@ -237,7 +238,9 @@ __global__ void __launch_bounds__(kT6Warps * 32) gemm_t6_kernel(T6Params p) {
 #pragma unroll
       for (int i = 0; i < 4; i++) {
         const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = (i & 2) ? row1 : row0;
-        if (tok < p.m && row < p.n) store_y<OUT>(p.y, (p.tok0 + tok) * p.n + row, acc[mt][i]);
+        if (tok < p.m && row < p.n)
+          store_y<OUT>(p.y, (p.tok0 + tok) * p.n + row,
+                       acc[mt][i] + residual_at<OUT>(p.res, (p.tok0 + tok) * p.n + row));
       }
   }
 }
@@ -290,19 +293,19 @@ bool gemv_stream_supported(int64_t m, int64_t spg);
 int64_t gemv_stream_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
 int gemv_stream_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
                        const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
-                       int, void*, cudaStream_t);
+                       int, void*, const void*, cudaStream_t);
 
 int64_t tc_act_m_pad(int64_t m);
 bool gemv_dyn_supported(int64_t m, int64_t spg);
 int64_t gemv_dyn_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
 int gemv_dyn_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
                     const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
-                    int, void*, cudaStream_t);
+                    int, void*, const void*, cudaStream_t);
 bool gemm_tc_supported(int64_t m, int64_t m_pad, int64_t spg);
 int64_t gemm_tc_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
 int gemm_tc_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
                    const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*, int,
-                   void*, cudaStream_t);
+                   void*, const void*, cudaStream_t);
 
 // FLEXQ_DISABLE_TC=1 routes M > 16 to the mma.sync kernel (A/B runs)
 static bool tc_enabled() {
@@ -338,7 +341,8 @@ int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int kspli
 int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
                    const uint32_t* act_frag, const float* act_scale, const int32_t* act_corr,
                    int64_t m, int64_t m_pad, int64_t n, int64_t k, int64_t gs, int32_t* partials,
-                   void* y, int out_dtype, void* workspace, int ksplit, cudaStream_t st) {
+                   void* y, int out_dtype, void* workspace, int ksplit, const void* residual,
+                   cudaStream_t st) {
   if (m < 1 || n < 1 || k < 1 || gs < 1) {
     set_error("gemm_t6: dims must be positive, got m=%lld n=%lld k=%lld group=%lld",
               (long long)m, (long long)n, (long long)k, (long long)gs);
@@ -362,15 +366,15 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   // decode regime, one group per k-block: dynamically scheduled pieces (gemv_dyn.cu)
   if (ksplit == 0 && gemv_dyn_supported(m, G.spg) && workspace)
     return gemv_dyn_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
-                           gs, partials, y, out_dtype, workspace, st);
+                           gs, partials, y, out_dtype, workspace, residual, st);
   // decode regime: the persistent TMA-fed streaming kernel (gemv_stream.cu)
   if (ksplit <= 0 && gemv_stream_supported(m, G.spg) && (workspace || !fast))
     return gemv_stream_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
-                              gs, partials, y, out_dtype, workspace, st);
+                              gs, partials, y, out_dtype, workspace, residual, st);
   // batched regime: tcgen05.mma kind::i8 with TMEM accumulators (gemm_tc.cu)
   if (ksplit == 0 && tc_enabled() && gemm_tc_supported(m, m_pad, G.spg) && (workspace || !fast))
     return gemm_tc_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k, gs,
-                          partials, y, out_dtype, workspace, st);
+                          partials, y, out_dtype, workspace, residual, st);
   if (ksplit <= 0) ksplit = auto_ksplit_t6(G.rt, G.kb);
   if (ksplit > 65535) ksplit = 65535;
   if (ksplit > 1 && fast && !workspace) {
@@ -401,6 +405,7 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
                                                          ws_counters_offset(ksplit, m_pad, G.rt))
                            : nullptr;
     p.ksplit = ksplit;
+    p.res = residual;
     const int mtiles = (int)cdiv(mc, kTokTile);
     if (mtiles <= 1) dispatch_t6<1>(p, scale_f16, trace, fast, out_dtype, st);
     else if (mtiles <= 2) dispatch_t6<2>(p, scale_f16, trace, fast, out_dtype, st);

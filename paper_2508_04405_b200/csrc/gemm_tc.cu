@@ -190,6 +190,7 @@ struct TcParams {
   void* y;
   float* ws_part;
   unsigned* counters;
+  const void* res;       // optional residual added at the store (same dtype/shape as y)
   long long* trace_clk;  // debug timeline of CTA 0 (FLEXQ_TC_TIMELINE), normally NULL
   int dbg;               // debug experiment bits (FLEXQ_TC_DBG), results invalid when set
 };
@@ -514,10 +515,11 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       for (int j = 0; j < CH; j++) {
         const int64_t m = tt * TN + hc * CH + j;
         if (m < p.m) {
+          const float v = a[j] + residual_at<OUT>(p.res, m * p.n + n_row);
           if constexpr (OUT == FLEXQ_OUT_F16)
-            reinterpret_cast<__half*>(p.y)[m * p.n + n_row] = __float2half_rn(a[j]);
+            reinterpret_cast<__half*>(p.y)[m * p.n + n_row] = __float2half_rn(v);
           else
-            reinterpret_cast<float*>(p.y)[m * p.n + n_row] = a[j];
+            reinterpret_cast<float*>(p.y)[m * p.n + n_row] = v;
         }
       }
     };
@@ -673,10 +675,11 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       for (int j = 0; j < 16; j++) {
         const int64_t m = tt * TN + c0 + j;
         if (m < p.m) {
+          const float v = a[j] + residual_at<OUT>(p.res, m * p.n + n_row);
           if constexpr (OUT == FLEXQ_OUT_F16)
-            reinterpret_cast<__half*>(p.y)[m * p.n + n_row] = __float2half_rn(a[j]);
+            reinterpret_cast<__half*>(p.y)[m * p.n + n_row] = __float2half_rn(v);
           else
-            reinterpret_cast<float*>(p.y)[m * p.n + n_row] = a[j];
+            reinterpret_cast<float*>(p.y)[m * p.n + n_row] = v;
         }
       }
     };
@@ -962,7 +965,7 @@ extern "C" int flexq_debug_tc_timeline(long long* host, int max_entries) {
 int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const uint32_t* act_frag,
                    const float* xs, const int32_t* corr, int64_t m, int64_t m_pad, int64_t n,
                    int64_t k, int64_t gs, int32_t* partials, void* y, int out_dtype,
-                   void* workspace, cudaStream_t st) {
+                   void* workspace, const void* residual, cudaStream_t st) {
   T6Geom G(n, k, gs);
   if (!gemm_tc_supported(m, m_pad, G.spg)) {
     set_error("gemm_tc: unsupported m=%lld m_pad=%lld group_size=%lld", (long long)m,
@@ -992,6 +995,7 @@ int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const 
   p.geo = G;
   p.partials = partials;
   p.y = y;
+  p.res = residual;
   if (getenv("FLEXQ_TC_DBG")) p.dbg = atoi(getenv("FLEXQ_TC_DBG"));
   if (getenv("FLEXQ_TC_TIMELINE")) {
     if (!g_tl) cudaMalloc(&g_tl, (4 * kTlUnits * 4 + 4 * 1024) * sizeof(long long));

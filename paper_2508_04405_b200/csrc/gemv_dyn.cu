@@ -31,6 +31,7 @@ struct DynParams {
   float* slots;         // [rg][ppr][4][MT][4][32] fp32 piece partials
   unsigned* counters;   // [rg] pieces finished (left zeroed)
   unsigned* queue;      // [2]: next dynamic piece - nw, finished warps (left zeroed)
+  const void* res;      // optional residual added at the store
 };
 
 template <int MT, bool SF16>
@@ -164,7 +165,8 @@ __global__ void __launch_bounds__(kDWarps * 32, MT == 1 ? 3 : 2) gemv_t6_dyn_ker
         for (int i = 0; i < 4; i++) {
           if (ONE && (i & 1)) continue;
           const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = row0 + ((i & 2) ? 8 : 0);
-          if (tok < p.m && row < p.n) dyn_store<OUT>(p.y, tok * p.n + row, acc[r][mt][i]);
+          if (tok < p.m && row < p.n)
+            dyn_store<OUT>(p.y, tok * p.n + row, acc[r][mt][i] + residual_at<OUT>(p.res, tok * p.n + row));
         }
     }
   };
@@ -423,7 +425,7 @@ static int dispatch_dyn(const DynParams& p, bool sf16, bool trace, bool fast, in
 int gemv_dyn_launch(const uint32_t* t6, const void* wscale, int scale_f16, const uint32_t* act_frag,
                     const float* xs, const int32_t* corr, int64_t m, int64_t m_pad, int64_t n,
                     int64_t k, int64_t gs, int32_t* partials, void* y, int out_dtype,
-                    void* workspace, cudaStream_t st) {
+                    void* workspace, const void* residual, cudaStream_t st) {
   T6Geom G(n, k, gs);
   if (!gemv_dyn_supported(m, G.spg) || !workspace) {
     set_error("gemv_dyn: unsupported m=%lld group_size=%lld (or no workspace)", (long long)m,
@@ -440,6 +442,7 @@ int gemv_dyn_launch(const uint32_t* t6, const void* wscale, int scale_f16, const
   p.geo = G;
   p.partials = partials;
   p.y = y;
+  p.res = residual;
   const int mt = m <= 8 ? 1 : 2;
   char* ws = reinterpret_cast<char*>(workspace);
   p.slots = reinterpret_cast<float*>(ws);

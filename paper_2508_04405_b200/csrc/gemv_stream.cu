@@ -46,6 +46,7 @@ struct StreamParams {
   void* y;
   float* ws_part;
   unsigned* counters;
+  const void* res;  // optional residual added at the store (same dtype/shape as y)
   int rev;
   long long* tl;  // debug timeline (FLEXQ_GEMV_TIMELINE): per warp [start, pdl done, first data, loop done, end]
 };
@@ -323,7 +324,8 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
         for (int i = 0; i < 4; i++) {
           if (ONE && (i & 1)) continue;
           const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = row0 + ((i & 2) ? 8 : 0);
-          if (tok < p.m && row < p.n) store_out<OUT>(p.y, tok * p.n + row, acc[r][mt][i]);
+          if (tok < p.m && row < p.n)
+            store_out<OUT>(p.y, tok * p.n + row, acc[r][mt][i] + residual_at<OUT>(p.res, tok * p.n + row));
         }
     }
   };
@@ -528,7 +530,7 @@ int64_t gemv_stream_workspace(int64_t m, int64_t n, int64_t k, int64_t gs) {
 int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
                        const uint32_t* act_frag, const float* xs, const int32_t* corr, int64_t m,
                        int64_t m_pad, int64_t n, int64_t k, int64_t gs, int32_t* partials, void* y,
-                       int out_dtype, void* workspace, cudaStream_t st) {
+                       int out_dtype, void* workspace, const void* residual, cudaStream_t st) {
   T6Geom G(n, k, gs);
   const int mode = stream_mode(G.spg);
   if (m > 16 || mode < 0) {
@@ -557,6 +559,7 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   p.geo = G;
   p.partials = partials;
   p.y = y;
+  p.res = residual;
   if (getenv("FLEXQ_GEMV_REV")) p.rev = 1;
   if (getenv("FLEXQ_GEMV_TIMELINE")) {
     static long long* tlbuf = nullptr;

@@ -70,8 +70,9 @@ class FlexQLinear:
         return self.t6.numel() * 4 + self.wscale.numel() * self.wscale.element_size()
 
     # -- forward --------------------------------------------------------------------------
-    def forward(self, x, out=None):
-        """x: fp16 CUDA [M, K] -> fp16 CUDA [M, N] (no host sync)."""
+    def forward(self, x, out=None, residual=None):
+        """x: fp16 CUDA [M, K] -> fp16 CUDA [M, N] (no host sync).  ``residual`` (fp16
+        [M, N], may be ``out`` itself) is added in the GEMM epilogue."""
         t = _dev.torch()
         if x.dim() != 2 or x.shape[1] != self.k:
             raise ShapeError(f"activation shape {tuple(x.shape)} does not match K={self.k}")
@@ -82,10 +83,10 @@ class FlexQLinear:
         if out is None:
             out = t.empty((m, self.n), dtype=t.float16, device=self.device)
         act, ws = self.buffers(m)
-        _lib.check(_lib.lib().flexq_linear_forward(
+        _lib.check(_lib.lib().flexq_linear_forward_ex(
             _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), self.activation_bits,
             _lib.ptr(x), m, self.n, self.k, self.group_size, _lib.ptr(out), _lib.ptr(act),
-            _lib.ptr(ws), _lib.ptr(self.flag), _lib.stream()))
+            _lib.ptr(ws), _lib.ptr(self.flag), _lib.ptr(residual), _lib.stream()))
         return out
 
     __call__ = forward
@@ -101,16 +102,16 @@ class FlexQLinear:
         base = act.data_ptr()
         return base, base + frag, base + frag + vec, m_pad
 
-    def gemm_only(self, m: int, out):
+    def gemm_only(self, m: int, out, residual=None):
         """Re-run only the T6 GEMM on the activations quantized by the last forward(m).
 
         Used by bench.py to time the dominant kernel alone (roofline)."""
         frag, xs, corr, m_pad = self._act_views(m)
         _, ws = self.buffers(m)
-        _lib.check(_lib.lib().flexq_gemm_t6(
+        _lib.check(_lib.lib().flexq_gemm_t6_ex(
             _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), frag, xs, corr, m,
             m_pad, self.n, self.k, self.group_size, None, _lib.ptr(out), _lib.OUT_F16,
-            _lib.ptr(ws), 0, _lib.stream()))
+            _lib.ptr(ws), 0, _lib.ptr(residual), _lib.stream()))
         return out
 
     def check_errors(self) -> None:

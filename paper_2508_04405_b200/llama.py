@@ -10,9 +10,9 @@ Per layer and token, all on the caller's stream (one CUDA graph per decode step)
   fused RMSNorm -> A6 quantize      (flexq_rmsnorm_quantize)
   qkv_proj W6A6 GEMV                 (FlexQLinear.gemm_only: q, k, v fused, N = 3 * hidden)
   RoPE + KV-cache append, attention  (flexq_rope_kv_append, flexq_attn_decode)
-  o_proj W6A6 (quantize + GEMV), residual add
+  o_proj W6A6 (quantize + GEMV, residual add fused into the epilogue)
   fused RMSNorm -> A6 quantize, gate_up W6A6 GEMV (gate and up fused, N = 2 * ffn)
-  fused SiLU(gate) * up -> A8 quantize, down_proj W6A8 GEMV, residual add
+  fused SiLU(gate) * up -> A8 quantize, down_proj W6A8 GEMV (+ fused residual add)
 then the final RMSNorm, an fp16 lm_head and a greedy argmax on the device.
 """
 from __future__ import annotations
@@ -151,15 +151,13 @@ class FlexQLlamaDecoder:
                 _lib.ptr(self.q), _lib.ptr(self.k_cache[li]), _lib.ptr(self.v_cache[li]),
                 _lib.ptr(self.pos), _lib.ptr(self.attn), B, cfg.heads, cfg.head_dim, self.max_len,
                 _lib.stream()))
-            lay.o.forward(self.attn, out=self.o_out)
-            self.x.add_(self.o_out)
+            lay.o.forward(self.attn, out=self.x, residual=self.x)  # x += o(attn), fused
             h2 = t.empty_like(self.x) if rec is not None else None
             self._fused_quant("rmsnorm", self.x, lay.gate_up, cfg.hidden, lay.norm2, h2)
             lay.gate_up.gemm_only(B, self.gu)
             h3 = t.empty((B, cfg.ffn), dtype=t.float16, device=self.device) if rec is not None else None
             self._fused_quant("silu", self.gu, lay.down, cfg.ffn, None, h3)
-            lay.down.gemm_only(B, self.d_out)
-            self.x.add_(self.d_out)
+            lay.down.gemm_only(B, self.x, residual=self.x)  # x += down(h), fused
             if rec is not None:
                 for kind, h in zip(_Layer.KINDS, (h1, self.attn.clone(), h2, h3)):
                     rec[kind].append(h)

@@ -112,3 +112,21 @@ def test_tc_public_api(m):
     y = lin(torch.from_numpy(x).cuda()).float().cpu().numpy()
     assert max_rel(y, y_ref) <= FP16_TOL
     lin.check_errors()
+
+
+@pytest.mark.parametrize("m", [1, 8, 33, 100])
+def test_fused_residual_epilogue(m):
+    """y = x W^T + r in the GEMM epilogue (GEMV for M <= 16, tcgen05 above), r aliasing y."""
+    n, k = 1024, 2048
+    g = torch.Generator(device="cuda").manual_seed(m)
+    lin = fq.FlexQLinear(torch.randn((n, k), generator=g, device="cuda").half(), activation_bits=6)
+    x = torch.randn((m, k), generator=g, device="cuda").half()
+    r = torch.randn((m, n), generator=g, device="cuda").half()
+    y0 = lin(x).float()
+    y = r.clone()
+    lin.forward(x, out=y, residual=y)  # in place: y <- x W^T + y
+    ref = y0 + r.float()
+    assert torch.allclose(y.float(), ref, atol=1e-2, rtol=2e-3)
+    y2 = torch.empty_like(r)
+    lin.forward(x, out=y2, residual=r)  # separate residual buffer
+    assert torch.equal(y2, y)
