@@ -123,10 +123,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680)  // suspend-time hint (ns): sleep in hardware, do not spin
+      "r"(parity)  // (a suspend-time hint measured +40 cycles per completed wait, tools/probe/mbar_lat.cu)
       : "memory");
 }
 // 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`

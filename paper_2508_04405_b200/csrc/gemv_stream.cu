@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   const int gq = lane >> 2, t = lane & 3;
   const int64_t gw = (int64_t)blockIdx.x * kSWarps + warp;
   if (gw >= p.nw) return;  // warp-uniform; no CTA-wide barriers below
-  if (p.tl && lane == 0) p.tl[gw * 5 + 0] = gv_timer();
+  if (p.tl && lane == 0) p.tl[gw * 8 + 0] = gv_timer();
   uint8_t* ring = smem + warp * (S * UB);
   uint64_t* bar = bars[warp];
   const int64_t gr = p.rev ? p.nw - 1 - gw : gw;  // debug: reversed range assignment
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   }
   __syncwarp();
   const uint64_t pol_w = l2_policy_evict_first(), pol_a = l2_policy_evict_last();
+  if (p.tl && lane == 0) p.tl[gw * 8 + 1] = gv_timer();
 
   // No integer division on the per-unit path: (row group, k-block, group) advance
   // incrementally.  spu = k-blocks per group (MODE 2), gshift = log2 groups per k-block (MODE 1).
@@ -180,9 +181,10 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
       else if (MODE == 2 && ++prem == spu) { prem = 0; pg++; }
     }
   }
+  if (p.tl && lane == 0) p.tl[gw * 8 + 2] = gv_timer();
   pdl_wait();
   pdl_launch_dependents();
-  if (p.tl && lane == 0) p.tl[gw * 5 + 1] = gv_timer();
+  if (p.tl && lane == 0) p.tl[gw * 8 + 3] = gv_timer();
   if (lane == 0) {
     for (int s = 0; s < pro; s++) {
       issue(iu, irg, ikb, group_lo(ikb, ig), s, 1);
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   for (int64_t u = u0; u < u1; u++) {
     const int g_lo = group_lo(kb, gdiv);
     mbar_wait(&bar[s], parity);
-    if (p.tl && lane == 0 && u == u0) p.tl[gw * 5 + 2] = gv_timer();
+    if (p.tl && lane == 0 && u == u0) p.tl[gw * 8 + 4] = gv_timer();
     const uint8_t* st = ring + s * UB;
     uint4 bv[MT][2], w[4][3];
 #pragma unroll
@@ -436,9 +438,9 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
       drain_groups(cur_rg, g, sw, sx);
     }
   }
-  if (p.tl && lane == 0) p.tl[gw * 5 + 3] = gv_timer();
+  if (p.tl && lane == 0) p.tl[gw * 8 + 5] = gv_timer();
   if (kb != 0) flush(cur_rg);  // (kb == 0: the last row group was already published)
-  if (p.tl && lane == 0) p.tl[gw * 5 + 4] = gv_timer();
+  if (p.tl && lane == 0) p.tl[gw * 8 + 7] = gv_timer();
 }
 
 // ---- host side ------------------------------------------------------------------------------
@@ -451,7 +453,7 @@ static int stream_mode(int64_t spg) {
 
 static long long* g_gemv_tl = nullptr;
 extern "C" int flexq_debug_gemv_timeline(long long* host, int max_entries) {
-  const int n = 148 * 16 * 5;
+  const int n = 148 * 16 * 8;
   if (!g_gemv_tl || max_entries < n) return 0;
   cudaDeviceSynchronize();
   cudaMemcpy(host, g_gemv_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -563,8 +565,8 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   if (getenv("FLEXQ_GEMV_REV")) p.rev = 1;
   if (getenv("FLEXQ_GEMV_TIMELINE")) {
     static long long* tlbuf = nullptr;
-    if (!tlbuf) cudaMalloc(&tlbuf, 148 * 16 * 5 * sizeof(long long));
-    cudaMemsetAsync(tlbuf, 0, 148 * 16 * 5 * sizeof(long long), st);
+    if (!tlbuf) cudaMalloc(&tlbuf, 148 * 16 * 8 * sizeof(long long));
+    cudaMemsetAsync(tlbuf, 0, 148 * 16 * 8 * sizeof(long long), st);
     p.tl = tlbuf;
     g_gemv_tl = tlbuf;
   }

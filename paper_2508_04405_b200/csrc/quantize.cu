@@ -271,11 +271,75 @@ int popcount_and_launch(const uint8_t* a, const uint8_t* b, int64_t nbytes, int6
   return FLEXQ_OK;
 }
 
+// ---- fast path: fp16 input, group = 128 = one k-block, K % 128 == 0 -----------------
+// One warp per (row, group); lane L owns the 4 consecutive columns 4L..4L+3, i.e. 4
+// consecutive bytes of the activation operand (k-step L/8, k-core 2(L%4) + (L/4)%2), so
+// every lane issues one 8 B load and one 4 B store and no address needs a 64-bit division.
+// Same float64 arithmetic as quantize_warp_kernel: bit-identical codes / scales.
+__device__ __forceinline__ int code_of(double v, double s, int bits) {
+  return isfinite(v) ? quant_one(v, s, bits) : 0;
+}
+
+__global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t ng = A.ng;
+  if (item >= A.rows * ng) return;
+  const int64_t r = item / ng, g = item - r * ng;  // once per warp
+  const __half* xr = reinterpret_cast<const __half*>(A.x) + r * A.cols + g * 128 + lane * 4;
+  const uint2 raw = *reinterpret_cast<const uint2*>(xr);
+  const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+  const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+  const double v[4] = {(double)f01.x, (double)f01.y, (double)f23.x, (double)f23.y};
+  bool finite = true;
+  float peak = 0.f;  // max of fp16 magnitudes: exact in fp32
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    finite &= isfinite(v[i]);
+    peak = fmaxf(peak, fabsf((float)v[i]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+  if (!__all_sync(0xffffffffu, finite)) {
+    if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
+    peak = 0.f;
+  }
+  const double sc = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
+  int c[4], csum = 0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    c[i] = code_of(v[i], sc, A.bits);
+    csum += c[i];
+  }
+  const uint32_t word = (uint32_t)(c[0] & 0xff) | ((uint32_t)(c[1] & 0xff) << 8) |
+                        ((uint32_t)(c[2] & 0xff) << 16) | ((uint32_t)(c[3] & 0xff) << 24);
+  if (A.codes) *reinterpret_cast<uint32_t*>(A.codes + r * A.cols + g * 128 + lane * 4) = word;
+  if (A.act_frag) {
+    const int jj = lane >> 3, h = (lane >> 2) & 1, t = lane & 3;
+    const int64_t off = ((g * (A.m_pad >> 3) + (r >> 3)) * 8 + 2 * t + h) * 128 + (r & 7) * 16 + jj * 4;
+    *reinterpret_cast<uint32_t*>(A.act_frag + off) = word;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  if (lane == 0) {
+    if (A.scales) A.scales[r * ng + g] = sc;
+    if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)sc;
+    if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
+  }
+}
+
 constexpr int64_t kWarpGroupMax = 1024;
 
 template <int DT>
 static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
   const int64_t items = A.rows * A.ng;
+  if (DT == FLEXQ_DT_F16 && A.gs == 128 && A.cols % 128 == 0 &&
+      reinterpret_cast<uintptr_t>(A.x) % 8 == 0) {
+    launch_pdl(quantize_g128_kernel, dim3((unsigned)cdiv(items, 8)), dim3(256), 0, st, A);
+    return;
+  }
   if (A.gs <= kWarpGroupMax || A.cols <= kWarpGroupMax) {
     const int warps = 8;
     launch_pdl(quantize_warp_kernel<DT>, dim3((unsigned)cdiv(items, warps)), dim3(warps * 32), 0,
@@ -400,6 +464,46 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_quant_kernel(FusedQuan
   }
   const int64_t g = (int64_t)blockIdx.y * kFusedWarps + warp;
   if (g >= A.ng) return;
+  if (A.gs == 128 && (K & 127) == 0) {
+    // lane L: the 4 consecutive columns 4L..4L+3 -> 4 consecutive operand bytes, one store
+    const int64_t c0 = g * 128 + lane * 4;
+    double v[4];
+    bool finite = true;
+    float peak = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const __half hv = fused_h(F, xr, c0 + i, inv);
+      if (F.h_out) F.h_out[r * K + c0 + i] = hv;
+      v[i] = (double)__half2float(hv);
+      finite &= isfinite(v[i]);
+      peak = fmaxf(peak, fabsf(__half2float(hv)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    if (!__all_sync(0xffffffffu, finite)) {
+      if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
+      peak = 0.f;
+    }
+    const double s = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
+    int csum = 0;
+    uint32_t word = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int code = isfinite(v[i]) ? quant_one(v[i], s, A.bits) : 0;
+      csum += code;
+      word |= (uint32_t)(code & 0xff) << (8 * i);
+    }
+    const int jj = lane >> 3, hh = (lane >> 2) & 1, t = lane & 3;
+    const int64_t off = ((g * (A.m_pad >> 3) + (r >> 3)) * 8 + 2 * t + hh) * 128 + (r & 7) * 16 + jj * 4;
+    *reinterpret_cast<uint32_t*>(A.act_frag + off) = word;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if (lane == 0) {
+      A.act_scale[g * A.m_pad + r] = (float)s;
+      A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
+    }
+    return;
+  }
   const int64_t lo = g * A.gs, hi = min(lo + A.gs, A.cols);
   double peak = 0.0;
   bool finite = true;

@@ -409,3 +409,39 @@ def test_70b_down_proj_full_size_properties():
     assert max_rel(y, y_ref) <= FP16_TOL
     y4 = lin(xt * 4).float().cpu().numpy()  # codes identical, activation scales exactly x4
     assert np.array_equal(y4, 4 * y)
+
+
+def test_quantizer_fast_path_matches_generic():
+    """fp16 / group-128 fast kernel == the generic float64 kernel (fed the same values as
+    fp32) on every output, including exact ties, zeros, subnormals and an all-zero group."""
+    L = _lib.lib()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    m, k = 5, 1024
+    x = (torch.randn((m, k), generator=g, device="cuda") * 3).half()
+    x[0, :128] = 0                                              # all-zero group -> scale 1
+    x[1, 128:256] = torch.arange(128, device="cuda").half() * 0.5  # many exact half-step ties
+    x[2, 256:260] = torch.tensor([6e-8, -6e-8, 1e-5, 65504.0]).half()
+    x[3, 512:640] = torch.linspace(-31, 31, 128, device="cuda").half()
+    outs = []
+    for dt, src in ((_lib.DT_F16, x), (_lib.DT_F32, x.float())):
+        for bits in (6, 8):
+            m_pad = L.flexq_act_m_pad(m)
+            codes = torch.zeros((m, k), dtype=torch.int8, device="cuda")
+            scales = torch.zeros((m, k // 128), dtype=torch.float64, device="cuda")
+            frag = torch.zeros(L.flexq_act_frag_bytes(m_pad, k, 128) // 4, dtype=torch.int32,
+                               device="cuda")
+            xs = torch.zeros((k // 128, m_pad), dtype=torch.float32, device="cuda")
+            corr = torch.zeros((k // 128, m_pad), dtype=torch.int32, device="cuda")
+            flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+            _lib.check(L.flexq_quantize(_lib.ptr(src), dt, m, k, bits, 128, 1, _lib.ptr(codes),
+                                        _lib.ptr(scales), _lib.ptr(frag), _lib.ptr(xs),
+                                        _lib.ptr(corr), m_pad, _lib.ptr(flag), _lib.stream()))
+            outs.append((codes, scales, frag, xs, corr))
+    torch.cuda.synchronize()
+    for a, b in zip(outs[:2], outs[2:]):
+        for ta, tb in zip(a, b):
+            assert torch.equal(ta, tb)
+    # and against the reference restatement on the host
+    xc, xsc = c_oracle.quantize(x.cpu().numpy(), 6, 128, True)
+    assert np.array_equal(outs[0][0].cpu().numpy(), xc)
+    assert np.array_equal(outs[0][1].cpu().numpy(), xsc)

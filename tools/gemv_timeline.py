@@ -22,17 +22,20 @@ def main():
         lay.forward(x, out=out)
     torch.cuda.synchronize()
     lay.gemm_only(m, out)
-    nall = 148 * 16 * 5
+    nall = 148 * 16 * 8
     buf = (ctypes.c_longlong * nall)()
     fn = _lib.lib().flexq_debug_gemv_timeline
     fn.restype = ctypes.c_int
     fn(buf, nall)
-    a = np.frombuffer(buf, dtype=np.int64).reshape(-1, 5)
+    a = np.frombuffer(buf, dtype=np.int64).reshape(-1, 8)
     a = a[a[:, 0] > 0]
     t0 = a[:, 0].min()
     d = (a - t0) / 1e3
     print(f"{n}x{k} m={m}: warps {len(a)}")
-    for i, name in enumerate(["start", "pdl_done", "first_data", "loop_done", "end"]):
+    for i, name in enumerate(["start", "init_done", "prologue", "pdl_done", "first_data",
+                              "loop_done", "-", "end"]):
+        if name == "-":
+            continue
         print(f"  {name:10s} min {d[:, i].min():7.2f}  median {np.median(d[:, i]):7.2f}  max {d[:, i].max():7.2f} us")
     per_cta(a)
 
@@ -40,7 +43,7 @@ def main():
 
 def per_cta(a, warps_per_cta=4):
     import numpy as np
-    dur = (a[:, 3] - a[:, 2]) / 1e3
+    dur = (a[:, 5] - a[:, 4]) / 1e3
     n = len(dur) // warps_per_cta * warps_per_cta
     c = dur[:n].reshape(-1, warps_per_cta).mean(1)
     print("  per-CTA loop us: " + " ".join(f"{v:.1f}" for v in c[:48]))

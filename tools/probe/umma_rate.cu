@@ -27,6 +27,7 @@ __global__ void probe(long long* out, int iters, int mode) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t holder;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar2[4], bar3[2], done[2];
   uint8_t* A = sm;             // 4 stages x 16 KB
   uint8_t* B = sm + 4 * 16384; // 4 stages x N*128
   for (int i = threadIdx.x; i < (4 * 16384 + 4 * N * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u;
@@ -34,7 +35,15 @@ __global__ void probe(long long* out, int iters, int mode) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&holder)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar))); }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar)));
+    for (int i = 0; i < 4; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 100000;" ::"r"(s32(&bar2[i])));
+    for (int i = 0; i < 2; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 100000;" ::"r"(s32(&bar3[i])));
+    for (int i = 0; i < 2; i++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&done[i])));
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(&done[i])));
+    }
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -51,6 +60,13 @@ __global__ void probe(long long* out, int iters, int mode) {
       for (int s = 0; s < 4; s++)
         mma(tmem + (it & 1) * N, ad + ((mode & 1) ? s * 2 : s * 16), bd + s * 16, idesc);
       if (mode & 2) { commit(&bar); wait(&bar, ph); ph ^= 1; }
+      if (mode & 4) {  // kernel-shaped sync per k-block (barriers pre-completed by a helper)
+        commit(&bar2[it & 3]);
+        commit(&bar3[it & 1]);
+        wait(&done[0], 0);
+        wait(&done[1], 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
     }
     commit(&bar); wait(&bar, ph);
     long long t1 = clock64();
@@ -64,8 +80,9 @@ template <int N>
 void run(long long* d) {
   const int smem = 4 * 16384 + 4 * N * 128;
   cudaFuncSetAttribute(probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* mn[] = {"A none ", "A sw128", "A none +commit/wait each", "A sw128+commit/wait each"};
-  for (int mode = 0; mode < 4; mode++) {
+  const char* mn[] = {"A none ", "A sw128", "A none +commit/wait each", "A sw128+commit/wait each",
+                      "", "A sw128 + kernel-shaped sync"};
+  for (int mode : {0, 1, 2, 3, 5}) {
     const int iters = 2000;
     probe<N><<<1, 128, smem>>>(d, iters, mode);
     cudaError_t e = cudaDeviceSynchronize();
