@@ -194,6 +194,15 @@ int flexq_silu_mul_quantize(const void* gate_up, int64_t x_stride, int64_t rows,
 int flexq_rope_kv_append(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache,
                          void* q_out, int64_t batch, int heads, int head_dim, int64_t max_len,
                          float theta, cudaStream_t stream);
+/* The whole attention block of a decode step in one kernel: RoPE + append (as above),
+ * attention, and the o_proj activation quantizer (head_dim 128 = group size, so head h of
+ * token b is group h): writes o_proj's operand (act_frag / act_scale / act_corr with
+ * m_pad = flexq_act_m_pad(batch)), bit-identical to flexq_quantize of the fp16 attention
+ * output, which is also stored to out[batch, heads * head_dim] when out is not NULL. */
+int flexq_attn_block(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache, void* out,
+                     int64_t batch, int heads, int head_dim, int64_t max_len, float theta,
+                     int bits, uint32_t* act_frag, float* act_scale, int32_t* act_corr,
+                     int64_t m_pad, uint32_t* flag, cudaStream_t stream);
 /* Single-query attention of q over cache positions [0, pos[b]] (head_dim 128). */
 int flexq_attn_decode(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
                       void* out, int64_t batch, int heads, int head_dim, int64_t max_len,

@@ -54,6 +54,8 @@ SIGNATURES = {
     "flexq_silu_mul_quantize": (i32, [vp, i64, i64, i64, i32, i64, vp, vp, vp, i64, vp, vp, vp]),
     "flexq_rope_kv_append": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, ctypes.c_float, vp]),
     "flexq_attn_decode": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, vp]),
+    "flexq_attn_block": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, ctypes.c_float, i32, vp, vp,
+                               vp, i64, vp, vp]),
 }
 
 _lib = None

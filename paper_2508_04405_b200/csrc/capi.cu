@@ -47,6 +47,8 @@ int rope_kv_append_launch(const void*, const int*, void*, void*, void*, int64_t,
                           float, cudaStream_t);
 int attn_decode_launch(const void*, const void*, const void*, const int*, void*, int64_t, int, int,
                        int64_t, cudaStream_t);
+int attn_block_launch(const void*, const int*, void*, void*, void*, int64_t, int, int, int64_t,
+                      float, int, uint32_t*, float*, int32_t*, int64_t, uint32_t*, cudaStream_t);
 int group_epilogue_launch(const int32_t*, const double*, const double*, int64_t, int64_t, int64_t,
                           double*, uint16_t*, cudaStream_t);
 
@@ -277,6 +279,14 @@ int flexq_attn_decode(const void* q, const void* k_cache, const void* v_cache, c
                       void* out, int64_t batch, int heads, int head_dim, int64_t max_len,
                       cudaStream_t stream) {
   return attn_decode_launch(q, k_cache, v_cache, pos, out, batch, heads, head_dim, max_len, stream);
+}
+
+int flexq_attn_block(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache, void* out,
+                     int64_t batch, int heads, int head_dim, int64_t max_len, float theta,
+                     int bits, uint32_t* act_frag, float* act_scale, int32_t* act_corr,
+                     int64_t m_pad, uint32_t* flag, cudaStream_t stream) {
+  return attn_block_launch(qkv, pos, k_cache, v_cache, out, batch, heads, head_dim, max_len, theta,
+                           bits, act_frag, act_scale, act_corr, m_pad, flag, stream);
 }
 
 }  // extern "C"

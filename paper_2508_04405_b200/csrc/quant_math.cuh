@@ -1,0 +1,32 @@
+// Scalar quantization math shared by every quantizer (quantize.py:29-36, 99-148):
+// float64 throughout, one correctly rounded IEEE operation per step, so codes and scales
+// are bit-identical with numpy.
+#pragma once
+#include "common.cuh"
+
+namespace flexq {
+
+__device__ __forceinline__ double group_scale(double peak, int bits, int fp16, uint32_t* flag) {
+  const double lim = (double)((1 << (bits - 1)) - 1);
+  double s = peak > 0.0 ? peak / lim : 1.0;
+  if (fp16) s = (double)__half2float(__double2half(s));
+  if (!(s > 0.0) && flag) atomicOr(flag, FLEXQ_FLAG_NONPOS_SCALE);
+  return s;
+}
+
+__device__ __forceinline__ int quant_one(double v, double s, int bits) {
+  const double lim = (double)((1 << (bits - 1)) - 1);
+  double q = v / s;
+  double a = floor(fabs(q) + 0.5);
+  if (a > lim) a = lim;
+  return q < 0.0 ? -(int)a : (int)a;
+}
+
+// Byte offset of the 4 consecutive operand bytes holding columns 4*lane .. 4*lane+3 of
+// group g (group = one 128-slot k-block) for token r.
+__device__ __forceinline__ int64_t operand_word_offset(int64_t g, int64_t r, int64_t m_pad, int lane) {
+  const int jj = lane >> 3, h = (lane >> 2) & 1, t = lane & 3;
+  return ((g * (m_pad >> 3) + (r >> 3)) * 8 + 2 * t + h) * 128 + (r & 7) * 16 + jj * 4;
+}
+
+}  // namespace flexq

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "quant_math.cuh"
 
 namespace flexq {
 
@@ -48,22 +49,6 @@ struct QuantArgs {
   // T6 geometry of the activation fragment layout
   int64_t spg, kb;
 };
-
-__device__ __forceinline__ double group_scale(double peak, int bits, int fp16, uint32_t* flag) {
-  const double lim = (double)((1 << (bits - 1)) - 1);
-  double s = peak > 0.0 ? peak / lim : 1.0;
-  if (fp16) s = (double)__half2float(__double2half(s));
-  if (!(s > 0.0) && flag) atomicOr(flag, FLEXQ_FLAG_NONPOS_SCALE);
-  return s;
-}
-
-__device__ __forceinline__ int quant_one(double v, double s, int bits) {
-  const double lim = (double)((1 << (bits - 1)) - 1);
-  double q = v / s;
-  double a = floor(fabs(q) + 0.5);
-  if (a > lim) a = lim;
-  return q < 0.0 ? -(int)a : (int)a;
-}
 
 // Byte of (token m, logical column c) in the activation operand:
 // [k-block][m_pad/8 token octets][8 k-cores][8 tokens][16 B] -- the K-major, no-swizzle

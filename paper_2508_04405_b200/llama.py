@@ -9,8 +9,8 @@ quantize.py:172-198), so its tokens/s is the FlexQ path's tokens/s.
 Per layer and token, all on the caller's stream (one CUDA graph per decode step):
   fused RMSNorm -> A6 quantize      (flexq_rmsnorm_quantize)
   qkv_proj W6A6 GEMV                 (FlexQLinear.gemm_only: q, k, v fused, N = 3 * hidden)
-  RoPE + KV-cache append, attention  (flexq_rope_kv_append, flexq_attn_decode)
-  o_proj W6A6 (quantize + GEMV, residual add fused into the epilogue)
+  RoPE + KV-cache append + attention + o_proj A6 quantize, one kernel (flexq_attn_block)
+  o_proj W6A6 GEMV (residual add fused into the epilogue)
   fused RMSNorm -> A6 quantize, gate_up W6A6 GEMV (gate and up fused, N = 2 * ffn)
   fused SiLU(gate) * up -> A8 quantize, down_proj W6A8 GEMV (+ fused residual add)
 then the final RMSNorm, an fp16 lm_head and a greedy argmax on the device.
@@ -143,15 +143,14 @@ class FlexQLlamaDecoder:
             h1 = t.empty_like(self.x) if rec is not None else None
             self._fused_quant("rmsnorm", self.x, lay.qkv, cfg.hidden, lay.norm1, h1)
             lay.qkv.gemm_only(B, self.qkv_out)
-            _lib.check(L.flexq_rope_kv_append(
+            # RoPE + KV append + attention + o_proj's activation quantizer, one kernel
+            frag, xs, corr, m_pad = lay.o._act_views(B)
+            _lib.check(L.flexq_attn_block(
                 _lib.ptr(self.qkv_out), _lib.ptr(self.pos), _lib.ptr(self.k_cache[li]),
-                _lib.ptr(self.v_cache[li]), _lib.ptr(self.q), B, cfg.heads, cfg.head_dim,
-                self.max_len, cfg.rope_theta, _lib.stream()))
-            _lib.check(L.flexq_attn_decode(
-                _lib.ptr(self.q), _lib.ptr(self.k_cache[li]), _lib.ptr(self.v_cache[li]),
-                _lib.ptr(self.pos), _lib.ptr(self.attn), B, cfg.heads, cfg.head_dim, self.max_len,
-                _lib.stream()))
-            lay.o.forward(self.attn, out=self.x, residual=self.x)  # x += o(attn), fused
+                _lib.ptr(self.v_cache[li]), _lib.ptr(self.attn) if rec is not None else None, B,
+                cfg.heads, cfg.head_dim, self.max_len, cfg.rope_theta, lay.o.activation_bits, frag,
+                xs, corr, m_pad, _lib.ptr(self.flag), _lib.stream()))
+            lay.o.gemm_only(B, self.x, residual=self.x)  # x += o(attn), residual fused
             h2 = t.empty_like(self.x) if rec is not None else None
             self._fused_quant("rmsnorm", self.x, lay.gate_up, cfg.hidden, lay.norm2, h2)
             lay.gate_up.gemm_only(B, self.gu)

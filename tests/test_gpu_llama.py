@@ -181,3 +181,38 @@ def test_tiny_decoder_graph_and_reference():
         # this random model, a wiring error shows up as O(1)
         assert err < 5e-2, f"step {pos}: rel err {err}"
         dec2.tokens.copy_(toks + 1)  # same inputs for both paths next step
+
+
+def test_attn_block_matches_separate_ops():
+    """flexq_attn_block == rope_kv_append + attn_decode (same caches, same output), and its
+    o_proj operand is bit-identical to flexq_quantize of that fp16 output."""
+    L = _lib.lib()
+    B, H, D, Lmax = 3, 4, 128, 32
+    g = torch.Generator(device="cuda").manual_seed(5)
+    caches = [torch.zeros((B, H, Lmax, D), dtype=torch.float16, device="cuda") for _ in range(4)]
+    q = torch.empty((B, H, D), dtype=torch.float16, device="cuda")
+    out_a = torch.empty((B, H * D), dtype=torch.float16, device="cuda")
+    out_b = torch.empty_like(out_a)
+    m_pad = L.flexq_act_m_pad(B)
+    frag = torch.zeros(L.flexq_act_frag_bytes(m_pad, H * D, 128) // 4, dtype=torch.int32, device="cuda")
+    xs = torch.zeros((H, m_pad), dtype=torch.float32, device="cuda")
+    corr = torch.zeros((H, m_pad), dtype=torch.int32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for step in range(7):
+        pos = torch.tensor([step, min(step, 3), step], dtype=torch.int32, device="cuda")
+        qkv = torch.randn((B, 3 * H * D), generator=g, device="cuda").half()
+        _lib.check(L.flexq_rope_kv_append(_lib.ptr(qkv), _lib.ptr(pos), _lib.ptr(caches[0]),
+                                          _lib.ptr(caches[1]), _lib.ptr(q), B, H, D, Lmax, 10000.0,
+                                          _lib.stream()))
+        _lib.check(L.flexq_attn_decode(_lib.ptr(q), _lib.ptr(caches[0]), _lib.ptr(caches[1]),
+                                       _lib.ptr(pos), _lib.ptr(out_a), B, H, D, Lmax, _lib.stream()))
+        _lib.check(L.flexq_attn_block(_lib.ptr(qkv), _lib.ptr(pos), _lib.ptr(caches[2]),
+                                      _lib.ptr(caches[3]), _lib.ptr(out_b), B, H, D, Lmax, 10000.0, 6,
+                                      _lib.ptr(frag), _lib.ptr(xs), _lib.ptr(corr), m_pad,
+                                      _lib.ptr(flag), _lib.stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(caches[0], caches[2]) and torch.equal(caches[1], caches[3])
+    assert torch.allclose(out_a.float(), out_b.float(), atol=2e-3, rtol=2e-3)
+    frag2, xs2, corr2, _ = _act_from_quantize(out_b, 6, None)
+    assert torch.equal(frag, frag2) and torch.equal(xs[:, :B], xs2[:, :B])
+    assert torch.equal(corr[:, :B], corr2[:, :B])
