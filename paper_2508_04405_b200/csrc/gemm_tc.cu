@@ -149,6 +149,11 @@ struct TcCfg {
   static constexpr int G = kRegAcc ? 1 : 2;                // event groups (TMEM-acc design)
   static constexpr int kDrainArrivals = kRegAcc ? 8 : 4;   // warps releasing one buffer
   static constexpr int NB = kRegAcc ? 8 : 2;               // TMEM drain buffers
+  // kRegAcc: the MMA and epilogue warps hand TMEM buffers over in pairs of consecutive drain
+  // events (one dfull commit / dempty wait per two groups), halving the synchronisation per
+  // k-block on both sides; EV = drain events per hand-over, NE = hand-over barriers
+  static constexpr int EV = kRegAcc ? 2 : 1;
+  static constexpr int NE = NB / EV;
   static constexpr int SS = 8;                     // scale/correction slot ring
   static constexpr int kRaw = 2 * kUnitBytes;
   static constexpr int kA = kTcRows * 128;
@@ -161,7 +166,7 @@ struct TcCfg {
   static constexpr int kOffTab = kOffB + SA * kB;
   static constexpr int kOffConst = kOffTab + SS * kTab;  // TN x 12582912.f (the seed as fp32)
   static constexpr int kOffBar = kOffConst + TN * 4;
-  static constexpr int kNumBars = 2 * SW + 2 * SA + 2 * NB + 2 * SS;
+  static constexpr int kNumBars = 2 * SW + 2 * SA + 2 * NE + 2 * SS;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static constexpr int kAccCols = kRegAcc ? 0 : G * TN;
   static constexpr uint32_t kTmemCols = NB * TN + kAccCols <= 128 ? 128 : NB * TN + kAccCols <= 256 ? 256 : 512;
@@ -316,8 +321,8 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
   uint64_t* afull = wempty + C::SW;   // A converted + B landed (4 converter warps + 1 TMA)
   uint64_t* aempty = afull + C::SA;   // stage consumed by the MMAs (tcgen05.commit)
   uint64_t* dfull = aempty + C::SA;
-  uint64_t* dempty = dfull + C::NB;
-  uint64_t* sfull = dempty + C::NB;
+  uint64_t* dempty = dfull + C::NE;
+  uint64_t* sfull = dempty + C::NE;
   uint64_t* sempty = sfull + C::SS;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + C::SS);
   volatile int* flush_flag = reinterpret_cast<volatile int*>(tmem_holder + 1);
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SW; i++) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], kTcConvWarps); }
     for (int i = 0; i < C::SA; i++) { mbar_init(&afull[i], kTcConvWarps + 1); mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < C::NB; i++) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], C::kDrainArrivals); }
+    for (int i = 0; i < C::NE; i++) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], C::kDrainArrivals); }
     for (int i = 0; i < C::SS; i++) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::kDrainArrivals); }
     fence_mbar_init();
   }
@@ -452,36 +457,45 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       }
     }
   } else if (warp == kTcWarpMma) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
-      int ai = 0, b = 0;
-      uint32_t aph = 0, dph = 0;
-      bool ev_open = false, ev_first = true;
-      for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
-        if (!ev_open) {
-          mbar_wait(&dempty[b], dph ^ 1u);
-          ev_open = true;
-          ev_first = true;
-        }
-        mbar_wait(&afull[ai], aph);
-        tc_fence_after();
+    // ===== MMA issuer: the whole warp walks the units (converged waits), one lane issues =====
+    int ai = 0, hb = 0, sub = 0;  // operand stage; hand-over buffer set, drain event within it
+    uint32_t aph = 0, dph = 0;
+    bool ev_open = false, ev_first = true;
+    for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+      const int b = hb * C::EV + sub;
+      if (lane == 0) tl_mark(p, 1, c.u - u0, 0);
+      if (!ev_open) {
+        if (sub == 0) mbar_wait(&dempty[hb], dph ^ 1u);
+        ev_open = true;
+        ev_first = true;
+      }
+      mbar_wait(&afull[ai], aph);
+      if (lane == 0) tl_mark(p, 1, c.u - u0, 1);
+      tc_fence_after();
+      if (lane == 0) {
         const uint64_t ad = umma_desc_sw128(smem_u32(smem + C::kOffA + ai * C::kA));
         const uint64_t bd = umma_desc(smem_u32(smem + C::kOffB + ai * C::kB));
 #pragma unroll
         for (int s = 0; s < 4; s++)  // K=32 step s: A +32 B (swizzled rows), B +256 B (2 cores)
           tc_mma_i8(tmem + b * TN, ad + (uint64_t)(s * 2), bd + (uint64_t)(s * 16), C::kIdesc,
                     (C::kRegAcc && ev_first && s == 0) ? 0u : 1u);
-        ev_first = false;
+        tl_mark(p, 1, c.u - u0, 2);
         tc_commit(&aempty[ai]);
-        if (c.drain_end(p)) {
-          tc_commit(&dfull[b]);
-          ev_open = false;
-          if (++b == C::NB) { b = 0; dph ^= 1u; }
-        }
-        if (++ai == C::SA) { ai = 0; aph ^= 1u; }
+        tl_mark(p, 1, c.u - u0, 3);
       }
-      cta_mark(p, 1, gtimer());
+      ev_first = false;
+      if (c.drain_end(p)) {
+        ev_open = false;
+        if (++sub == C::EV || c.tile_end(p)) {  // hand the set over (a tile end closes it early)
+          if (lane == 0) tc_commit(&dfull[hb]);
+          sub = 0;
+          if (++hb == C::NE) { hb = 0; dph ^= 1u; }
+        }
+      }
+      __syncwarp();
+      if (++ai == C::SA) { ai = 0; aph ^= 1u; }
     }
+    if (lane == 0) cta_mark(p, 1, gtimer());
   } else if (warp >= kTcWarpEpi0) {
     if constexpr (C::kRegAcc) {
     // ===== epilogue =====
@@ -524,7 +538,7 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       }
     };
 
-    int b = 0, si = 0;
+    int hb = 0, sub = 0, si = 0;  // hand-over set and drain event within it (C::EV per set)
     uint32_t dph = 0, sph = 0;
     int ev_kg0 = -1;        // kg of the event's first k-block
     for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
@@ -534,7 +548,9 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       ev_kg0 = -1;
       const int64_t tt = c.tt;
       const int64_t n_row = (int64_t)c.rt * kTcRows + rho;
-      mbar_wait(&dfull[b], dph);
+      const int b = hb * C::EV + sub;
+      const bool closes = sub + 1 == C::EV || c.tile_end(p);  // last event of the set
+      if (sub == 0) mbar_wait(&dfull[hb], dph);
       tc_fence_after();
       const uint8_t* slot = smem + C::kOffTab + si * C::kTab;
       const float* sx = reinterpret_cast<const float*>(slot) + hc * CH;
@@ -550,10 +566,10 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
           tmem_ld16x(tl + b * TN + w0 + 16 * h, *reinterpret_cast<uint32_t(*)[16]>(&v[16 * h]));
 #pragma unroll
         for (int h = 0; h < CW / 16; h++) tmem_wait_ld_r(*reinterpret_cast<uint32_t(*)[16]>(&v[16 * h]));
-        if (w0 + CW == CH) {  // the whole partial is in registers: release the TMEM buffer
+        if (closes && w0 + CW == CH) {  // the set's partials are in registers: release it
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&dempty[b]);
+          if (lane == 0) mbar_arrive(&dempty[hb]);
         }
         if (w0 == 0) mbar_wait(&sfull[si], sph);
         if constexpr (FAST) {
@@ -597,7 +613,12 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sempty[si]);
-      if (++b == C::NB) { b = 0; dph ^= 1u; }
+      if (closes) {
+        sub = 0;
+        if (++hb == C::NE) { hb = 0; dph ^= 1u; }
+      } else {
+        sub++;
+      }
       if (++si == C::SS) { si = 0; sph ^= 1u; }
 
       if (FAST && c.tile_end(p)) {

@@ -40,7 +40,7 @@ def main():
     for i in order:
         print(f"  slow cta: start {(cm[i,0]-t0g)/1e3:.2f} mma_done {(cm[i,1]-t0g)/1e3:.2f} end {(cm[i,2]-t0g)/1e3:.2f}")
     t0 = a[a > 0].min()
-    names = ["conv(start,wfull,aempty,done)", "mma(start,dempty,bfull,afull)",
+    names = ["conv(start,wfull,aempty,done)", "mma(start,afull_ok,mma_issued,commit_done)",
              "epi(sfull_ok,table_loaded,ld_done,chunk0_done)", "epi(start,dfull_ok,arrived)"]
     for r in range(4):
         print(names[r])
