@@ -60,6 +60,7 @@ __global__ void probe(long long* out, int iters, int mode) {
       for (int s = 0; s < 4; s++)
         mma(tmem + (it & 1) * N, ad + ((mode & 1) ? s * 2 : s * 16), bd + s * 16, idesc);
       if (mode & 2) { commit(&bar); wait(&bar, ph); ph ^= 1; }
+      if (mode & 8) commit(&bar2[it & 3]);  // commit only (async arrive), no wait
       if (mode & 4) {  // kernel-shaped sync per k-block (barriers pre-completed by a helper)
         commit(&bar2[it & 3]);
         commit(&bar3[it & 1]);
@@ -81,8 +82,8 @@ void run(long long* d) {
   const int smem = 4 * 16384 + 4 * N * 128;
   cudaFuncSetAttribute(probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* mn[] = {"A none ", "A sw128", "A none +commit/wait each", "A sw128+commit/wait each",
-                      "", "A sw128 + kernel-shaped sync"};
-  for (int mode : {0, 1, 2, 3, 5}) {
+                      "", "A sw128 + kernel-shaped sync", "", "", "", "A sw128 + commit only"};
+  for (int mode : {1, 3, 5, 9}) {
     const int iters = 2000;
     probe<N><<<1, 128, smem>>>(d, iters, mode);
     cudaError_t e = cudaDeviceSynchronize();
@@ -90,7 +91,7 @@ void run(long long* d) {
     long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     double cyc = (double)h / iters;
     double ops = 2.0 * 128 * N * 128;
-    printf("N=%3d %-26s %7.1f cycles/k-block  %6.0f ops/clk/SM (peak ~15500)\n", N, mn[mode], cyc, ops / cyc);
+    printf("N=%3d %-30s %7.1f cycles/k-block  %6.0f ops/clk/SM (peak ~15500)\n", N, mn[mode], cyc, ops / cyc);
   }
 }
 
