@@ -13,7 +13,8 @@ from __future__ import annotations
 
 from . import _dev, _lib
 from .errors import InvalidInputError, ShapeError
-from .quantize import DEFAULT_GROUP_SIZE, DEFAULT_POLICY, BitPolicy, quantize
+from .packing import PackedTensor
+from .quantize import DEFAULT_GROUP_SIZE, DEFAULT_POLICY, BitPolicy, QuantTensor, quantize
 from .quantize import activation_bits as policy_bits
 
 
@@ -34,15 +35,20 @@ class FlexQLinear:
             raise InvalidInputError(f"FlexQLinear packs at most 6-bit weights, got {weight_bits}")
         if activation_bits is None:
             activation_bits = policy_bits(layer_kind or "generic", policy)
-        t = _dev.torch()
-        self.weight_bits = weight_bits
-        self.activation_bits = int(activation_bits)
-        self.group_size = int(group_size)
-        self.fp16_scales = bool(fp16_scales)
-        self.layer_kind = layer_kind
         self.qweight = quantize(weight if _dev.is_torch(weight) else _dev.to_device(weight),
                                 weight_bits, group_size, fp16_scales=fp16_scales)
-        codes, scales = self.qweight.device_tensors()
+        self._setup(self.qweight, activation_bits, fp16_scales, layer_kind)
+
+    def _setup(self, qweight, activation_bits: int, fp16_scales: bool, layer_kind) -> None:
+        """Pack the quantized weight into the T6 stream (the offline half)."""
+        t = _dev.torch()
+        self.qweight = qweight
+        self.weight_bits = int(qweight.bits)
+        self.activation_bits = int(activation_bits)
+        self.group_size = int(qweight.group_size)
+        self.fp16_scales = bool(fp16_scales)
+        self.layer_kind = layer_kind
+        codes, scales = qweight.device_tensors()
         self.n, self.k = codes.shape
         from .engine import t6_pack_weights
 
@@ -51,6 +57,70 @@ class FlexQLinear:
         self.device = codes.device
         self._bufs: dict[int, tuple] = {}
         self.flag = t.zeros(1, dtype=t.int32, device=self.device)
+
+    # -- construction from reference artefacts ------------------
+    @classmethod
+    def from_quant(cls, q, activation_bits: int | None = None, layer_kind: str | None = None,
+                   policy: BitPolicy = DEFAULT_POLICY, fp16_scales: bool | None = None):
+        """Serve an already-quantized weight (a QuantTensor, e.g. ``fileio.read_quant`` of a
+        container written by the reference's ``bitserial quantize``) without re-quantizing.
+
+        The codes go straight into the T6 packer.  ``fp16_scales`` defaults to True exactly
+        when every scale is an fp16 value (then the 2-byte scale stream loses nothing), else
+        the kernel streams fp32 scales."""
+        if q.bits > 6:
+            raise InvalidInputError(f"FlexQLinear packs at most 6-bit weights, got {q.bits}")
+        if q.group_axis != 1:
+            raise InvalidInputError("weight groups must run along K (group_axis 1)")
+        _, scales = q.device_tensors()
+        if fp16_scales is None:
+            t = _dev.torch()
+            fp16_scales = bool(t.equal(scales.to(t.float16).to(t.float64), scales))
+        if activation_bits is None:
+            activation_bits = policy_bits(layer_kind or "generic", policy)
+        self = cls.__new__(cls)
+        self._setup(q, activation_bits, fp16_scales, layer_kind)
+        return self
+
+    @classmethod
+    def from_packed(cls, p, scales, group_size: int = DEFAULT_GROUP_SIZE, **kw):
+        """Serve FLXQ-P packed weight planes (a PackedTensor, e.g. ``fileio.read_packed`` of
+        ``bitserial pack`` output) with their per-(row, group) scales [N, n_groups].
+
+        The planes are unpacked on the GPU (csrc/pack.cu) and re-laid into the T6 stream;
+        no host pass over the weights."""
+        from .packing import unpack
+
+        if not p.signed:
+            raise InvalidInputError("weight planes must be signed (two's complement)")
+        if p.bits > 6:
+            raise InvalidInputError(f"FlexQLinear packs at most 6-bit weights, got {p.bits}")
+        t = _dev.torch()
+        codes = unpack(p, p.config).device_codes().to(t.int8)
+        sc = _dev.to_device(scales, t.float64)
+        q = QuantTensor(values=codes, scales=sc, bits=p.bits, group_size=group_size,
+                        _device=(codes, sc))
+        return cls.from_quant(q, **kw)
+
+    @classmethod
+    def load(cls, path: str, scales=None, group_size: int = DEFAULT_GROUP_SIZE, **kw):
+        """Build a layer from an FLXQ container: a quant tensor (kind 1) is served as is, a
+        packed tensor (kind 2) needs ``scales`` (an array, or the path of a quant or float
+        container holding them), a float tensor (kind 0) is quantized on the GPU."""
+        from . import fileio
+
+        obj = fileio.read(path)
+        if isinstance(obj, QuantTensor):
+            return cls.from_quant(obj, **kw)
+        if isinstance(obj, PackedTensor):
+            if scales is None:
+                raise InvalidInputError(f"{path}: packed weights need their scales")
+            if isinstance(scales, str):
+                s = fileio.read(scales)
+                scales, group_size = ((s.scales, s.group_size) if isinstance(s, QuantTensor)
+                                      else (s, group_size))
+            return cls.from_packed(obj, scales, group_size, **kw)
+        return cls(obj, group_size=group_size, **kw)
 
     # -- buffers ------------------------------------------------------------------------
     def buffers(self, m: int):
