@@ -16,8 +16,8 @@ __global__ void rope_kv_append_kernel(const __half* __restrict__ qkv, const int*
                                       __half* __restrict__ k_cache, __half* __restrict__ v_cache,
                                       __half* __restrict__ q_out, int H, int D, int Lmax,
                                       float theta) {
-  pdl_wait();
   pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.y, hh = blockIdx.x, i = threadIdx.x;  // i < D/2
   const int half = D / 2;
   const int p = pos[b];
@@ -50,8 +50,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_decode_kernel(
   constexpr int D = 128;
   __shared__ float sm_m[kAttnWarps], sm_l[kAttnWarps];
   __shared__ float sm_acc[kAttnWarps][D];
-  pdl_wait();
   pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.y, hh = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int len = pos[b] + 1;
@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_block_kernel(
   __shared__ float sm_m[kAttnWarps], sm_l[kAttnWarps];
   __shared__ float sm_acc[kAttnWarps][D];
   __shared__ __half sm_q[D];
-  pdl_wait();
   pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.y, hh = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int p = pos[b];

@@ -22,6 +22,11 @@ __device__ __forceinline__ int quant_one(double v, double s, int bits) {
   return q < 0.0 ? -(int)a : (int)a;
 }
 
+// Non-finite inputs quantize to 0 (the caller raises the flag and zeroes the peak).
+__device__ __forceinline__ int code_of(double v, double s, int bits) {
+  return isfinite(v) ? quant_one(v, s, bits) : 0;
+}
+
 // Byte offset of the 4 consecutive operand bytes holding columns 4*lane .. 4*lane+3 of
 // group g (group = one 128-slot k-block) for token r.
 __device__ __forceinline__ int64_t operand_word_offset(int64_t g, int64_t r, int64_t m_pad, int lane) {

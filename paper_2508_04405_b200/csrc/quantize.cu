@@ -260,10 +260,8 @@ int popcount_and_launch(const uint8_t* a, const uint8_t* b, int64_t nbytes, int6
 // One warp per (row, group); lane L owns the 4 consecutive columns 4L..4L+3, i.e. 4
 // consecutive bytes of the activation operand (k-step L/8, k-core 2(L%4) + (L/4)%2), so
 // every lane issues one 8 B load and one 4 B store and no address needs a 64-bit division.
-// Same float64 arithmetic as quantize_warp_kernel: bit-identical codes / scales.
-__device__ __forceinline__ int code_of(double v, double s, int bits) {
-  return isfinite(v) ? quant_one(v, s, bits) : 0;
-}
+// Same float64 arithmetic as quantize_warp_kernel (code_of: quant_math.cuh): bit-identical
+// codes / scales.
 
 __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
   pdl_wait();
@@ -411,8 +409,8 @@ __device__ __forceinline__ __half fused_h(const FusedQuantArgs& F, const __half*
 
 __global__ void __launch_bounds__(kFusedWarps * 32) fused_quant_kernel(FusedQuantArgs F) {
   __shared__ float red[kFusedWarps];
-  pdl_wait();
   pdl_launch_dependents();
+  pdl_wait();
   const QuantArgs& A = F.q;
   const int64_t r = blockIdx.x;
   const int K = (int)A.cols;
