@@ -60,9 +60,38 @@ static int check_chunk_m(int cm) {
   return FLEXQ_OK;
 }
 
+long long* dbg_trace_buf() {
+  static long long* buf = nullptr;
+  static const bool on = getenv("FLEXQ_TRACE") != nullptr;
+  if (on && !buf) {
+    cudaMalloc(&buf, (4 + 4 * kDbgCap) * sizeof(long long));
+    cudaMemset(buf, 0, 4 * sizeof(long long));
+  }
+  return buf;
+}
+
+long long dbg_next_launch() {
+  static long long n = 0;
+  return ++n;
+}
+
 }  // namespace flexq
 
 using namespace flexq;
+
+/* Debug: copy out and reset the event trace (FLEXQ_TRACE=1). Returns the record count. */
+extern "C" int flexq_debug_trace(long long* host, int max_records) {
+  long long* buf = dbg_trace_buf();
+  if (!buf) return 0;
+  cudaDeviceSynchronize();
+  unsigned long long n = 0;
+  cudaMemcpy(&n, buf, sizeof(n), cudaMemcpyDeviceToHost);
+  if (n > kDbgCap) n = kDbgCap;
+  if ((long long)n > max_records) n = max_records;
+  cudaMemcpy(host, buf + 4, n * 4 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaMemset(buf, 0, 4 * sizeof(long long));
+  return (int)n;
+}
 
 extern "C" {
 

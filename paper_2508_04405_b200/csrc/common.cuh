@@ -87,6 +87,27 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+// ---- debug event trace (FLEXQ_TRACE=1; tools/step_trace.py) -------------------------------
+// Kernels append {tag = launch << 8 | kind, t_start, t_mid, t_end} globaltimer records so a
+// multi-kernel step can be laid out on one time axis.  Off (nullptr) unless the env var is
+// set; never used on a production path.
+constexpr unsigned long long kDbgCap = 1 << 16;
+long long* dbg_trace_buf();  // host: device buffer, or nullptr when tracing is off
+long long dbg_next_launch();  // host: launch sequence number
+__device__ __forceinline__ long long dbg_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void dbg_record(long long* buf, long long tag, long long a, long long b,
+                                           long long c) {
+  const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(buf), 1ull);
+  if (i < kDbgCap) {
+    long long* r = buf + 4 + 4 * i;
+    r[0] = tag; r[1] = a; r[2] = b; r[3] = c;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {

@@ -48,7 +48,9 @@ struct StreamParams {
   unsigned* counters;
   const void* res;  // optional residual added at the store (same dtype/shape as y)
   int rev;
-  long long* tl;  // debug timeline (FLEXQ_GEMV_TIMELINE): per warp [start, pdl done, first data, loop done, end]
+  long long* dbg;  // FLEXQ_TRACE event buffer (debug)
+  long long dbg_tag;
+  long long* tl;  // debug timeline (FLEXQ_GEMV_TIMELINE): per warp [start, init, prologue, pdl done, first data, loop done, smid, end]
 };
 
 __device__ __forceinline__ long long gv_timer() {
@@ -101,7 +103,14 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   const int gq = lane >> 2, t = lane & 3;
   const int64_t gw = (int64_t)blockIdx.x * kSWarps + warp;
   if (gw >= p.nw) return;  // warp-uniform; no CTA-wide barriers below
-  if (p.tl && lane == 0) p.tl[gw * 8 + 0] = gv_timer();
+  const long long dt0 = p.dbg ? dbg_now() : 0;
+  long long dt1 = 0;
+  if (p.tl && lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.tl[gw * 8 + 0] = gv_timer();
+    p.tl[gw * 8 + 6] = smid;
+  }
   uint8_t* ring = smem + warp * (S * UB);
   uint64_t* bar = bars[warp];
   const int64_t gr = p.rev ? p.nw - 1 - gw : gw;  // debug: reversed range assignment
@@ -341,6 +350,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
     const int g_lo = group_lo(kb, gdiv);
     mbar_wait(&bar[s], parity);
     if (p.tl && lane == 0 && u == u0) p.tl[gw * 8 + 4] = gv_timer();
+    if (p.dbg && u == u0) dt1 = dbg_now();
     const uint8_t* st = ring + s * UB;
     uint4 bv[MT][2], w[4][3];
 #pragma unroll
@@ -441,6 +451,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   if (p.tl && lane == 0) p.tl[gw * 8 + 5] = gv_timer();
   if (kb != 0) flush(cur_rg);  // (kb == 0: the last row group was already published)
   if (p.tl && lane == 0) p.tl[gw * 8 + 7] = gv_timer();
+  if (p.dbg && lane == 0) dbg_record(p.dbg, p.dbg_tag, dt0, dt1, dbg_now());
 }
 
 // ---- host side ------------------------------------------------------------------------------
@@ -563,6 +574,8 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   p.y = y;
   p.res = residual;
   if (getenv("FLEXQ_GEMV_REV")) p.rev = 1;
+  p.dbg = dbg_trace_buf();
+  if (p.dbg) p.dbg_tag = dbg_next_launch() << 8 | 2;
   if (getenv("FLEXQ_GEMV_TIMELINE")) {
     static long long* tlbuf = nullptr;
     if (!tlbuf) cudaMalloc(&tlbuf, 148 * 16 * 8 * sizeof(long long));

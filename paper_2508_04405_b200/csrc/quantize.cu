@@ -48,6 +48,9 @@ struct QuantArgs {
   uint32_t* flag;
   // T6 geometry of the activation fragment layout
   int64_t spg, kb;
+  long long* dbg = nullptr;  // FLEXQ_TRACE event buffer (debug)
+  long long dbg_tag = 0;
+  int early = 0;  // experiment (FLEXQ_Q_EARLY): trigger dependents before waiting
 };
 
 // Byte of (token m, logical column c) in the activation operand:
@@ -264,8 +267,11 @@ int popcount_and_launch(const uint8_t* a, const uint8_t* b, int64_t nbytes, int6
 // codes / scales.
 
 __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
+  const long long dt0 = A.dbg ? dbg_now() : 0;
+  if (A.early) pdl_launch_dependents();
   pdl_wait();
-  pdl_launch_dependents();
+  if (!A.early) pdl_launch_dependents();
+  const long long dt1 = A.dbg ? dbg_now() : 0;
   const int lane = threadIdx.x & 31;
   const int64_t item = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t ng = A.ng;
@@ -310,6 +316,7 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
     if (A.scales) A.scales[r * ng + g] = sc;
     if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)sc;
     if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
+    if (A.dbg) dbg_record(A.dbg, A.dbg_tag, dt0, dt1, dbg_now());
   }
 }
 
@@ -363,6 +370,10 @@ int quantize_launch(const void* x, int dtype, int64_t rows, int64_t cols, int bi
   QuantArgs A{x, rows, cols, gs, geo.ng, bits, fp16_scales, codes, scales,
               reinterpret_cast<uint8_t*>(act_frag), act_scale, act_corr, m_pad, flag,
               geo.spg, geo.kb};
+  A.dbg = dbg_trace_buf();
+  static const int q_early = getenv("FLEXQ_Q_EARLY") ? 1 : 0;
+  A.early = q_early;
+  if (A.dbg) A.dbg_tag = dbg_next_launch() << 8 | 1;
   switch (dtype) {
     case FLEXQ_DT_F16: launch_quantize<FLEXQ_DT_F16>(A, st); break;
     case FLEXQ_DT_BF16: launch_quantize<FLEXQ_DT_BF16>(A, st); break;
