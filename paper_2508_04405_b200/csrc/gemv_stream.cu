@@ -31,8 +31,14 @@
 
 namespace flexq {
 
-constexpr int kSWarps = 4;  // warps per CTA (independent pipelines)
+constexpr int kSWarps = 4;  // warps per CTA in the default launch (independent pipelines)
+// Warps per CTA are a launch parameter (blockDim): the default packs 4-warp CTAs several to
+// an SM; FLEXQ_GEMV_WIDE=1 launches one CTA per SM holding all of that SM's warps.
+constexpr int kMaxWarpsMT1 = 12, kMaxWarpsMT2 = 8;
 constexpr int kMinUnitsPerWarp = 6;
+#ifndef FLEXQ_GEMV_FB1
+#define FLEXQ_GEMV_FB1 8  // split-fixup slots loaded per L2 round trip at M = 1
+#endif
 
 struct StreamParams {
   const uint8_t* t6;
@@ -91,17 +97,17 @@ __device__ __forceinline__ void store_out(void* y, int64_t i, float v) {
 // ONE: m == 1 (decode GEMV) -- only accumulator column 0 (c0, c2) is live, so the
 // dequant, the split fixup and the stores touch half the values.
 template <int MT, int MODE, bool SF16, bool TRACE, bool FAST, int OUT, int S, bool ONE>
-__global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
+__global__ void __launch_bounds__((MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2) * 32, 1)
     gemv_t6_stream_kernel(StreamParams p) {
   static_assert(!ONE || MT == 1, "ONE implies a single token tile");
   using L = StageLayout<MT, MODE, SF16>;
   constexpr int UB = L::kBytes;
   constexpr int SB = SF16 ? 4 : 8;  // bytes of one weight-scale pair
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[kSWarps][S];
+  const int nwc = blockDim.x >> 5;  // warps in this CTA
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, t = lane & 3;
-  const int64_t gw = (int64_t)blockIdx.x * kSWarps + warp;
+  const int64_t gw = (int64_t)blockIdx.x * nwc + warp;
   if (gw >= p.nw) return;  // warp-uniform; no CTA-wide barriers below
   const long long dt0 = p.dbg ? dbg_now() : 0;
   long long dt1 = 0;
@@ -112,7 +118,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
     p.tl[gw * 8 + 6] = smid;
   }
   uint8_t* ring = smem + warp * (S * UB);
-  uint64_t* bar = bars[warp];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + nwc * (S * UB)) + warp * S;
   const int64_t gr = p.rev ? p.nw - 1 - gw : gw;  // debug: reversed range assignment
   const int64_t u0 = gr * p.units / p.nw, u1 = (gr + 1) * p.units / p.nw;
 
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
 #pragma unroll
           for (int i = 0; i < 4; i++) acc[r][mt][i] = 0.f;
       // fixed order; FB contributors' slots in flight per L2 round trip
-      constexpr int FB = ONE ? 4 : 2;
+      constexpr int FB = ONE ? FLEXQ_GEMV_FB1 : (MT == 1 ? 4 : 2);  // measured best (tools/sweep.py)
       for (int64_t w = first; w <= last; w += FB) {
         float v[FB][4][MT][4];
 #pragma unroll
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(kSWarps * 32, MT == 1 ? 3 : 2)
   if (p.tl && lane == 0) p.tl[gw * 8 + 5] = gv_timer();
   if (kb != 0) flush(cur_rg);  // (kb == 0: the last row group was already published)
   if (p.tl && lane == 0) p.tl[gw * 8 + 7] = gv_timer();
-  if (p.dbg && lane == 0) dbg_record(p.dbg, p.dbg_tag, dt0, dt1, dbg_now());
+  if (p.dbg && lane == 0) dbg_record(p.dbg, p.dbg_tag | (gw << 40), dt0, dt1, dbg_now());
 }
 
 // ---- host side ------------------------------------------------------------------------------
@@ -487,26 +493,42 @@ template <int MT, int MODE, bool SF16, bool TRACE, bool FAST, int OUT, int S>
 static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
   auto kern = (MT == 1 && p.m == 1) ? gemv_t6_stream_kernel<MT, MODE, SF16, TRACE, FAST, OUT, S, MT == 1>
                                     : gemv_t6_stream_kernel<MT, MODE, SF16, TRACE, FAST, OUT, S, false>;
-  const int smem = kSWarps * S * StageLayout<MT, MODE, SF16>::kBytes;
+  constexpr int UB = StageLayout<MT, MODE, SF16>::kBytes;
+  constexpr int kMaxW = MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2;
+  static const bool wide = getenv("FLEXQ_GEMV_WIDE") != nullptr;
   static bool configured[2] = {false, false};  // one attribute call per instantiation
   const int ci = (MT == 1 && p.m == 1) ? 1 : 0;
   if (!configured[ci]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int cap = kMaxW * S * (UB + 8) < 227 * 1024 ? kMaxW * S * (UB + 8) : 227 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     if (e != cudaSuccess) return cuda_status(e, "gemv_stream attribute");
     configured[ci] = true;
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSWarps * 32, smem);
-  if (per_sm < 1) per_sm = 1;
-  if (per_sm > 4) per_sm = 4;  // workspace slots are sized for <= 16 warps per SM
-  int64_t warps = (int64_t)num_sms * per_sm * kSWarps;
+  int wpc = kSWarps, per_sm = 0;  // warps per CTA, CTAs per SM
+  if (wide) {  // one CTA per SM with as many warps as the SM's shared memory holds
+    wpc = (int)(227 * 1024 / (S * (UB + 8)));
+    if (wpc > kMaxW) wpc = kMaxW;
+    per_sm = 1;
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSWarps * 32,
+                                                  kSWarps * S * (UB + 8));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 4) per_sm = 4;  // workspace slots are sized for <= 16 warps per SM
+  }
+  const int smem = wpc * S * (UB + 8);
+  int64_t warps = (int64_t)num_sms * per_sm * wpc;
   // bounds the fixup fan-in; deep rings (small layers) spread the units thinner so that a
   // warp's whole range is in flight at once
-  const int64_t by_units = cdiv(p.units, S >= 4 ? 2 : kMinUnitsPerWarp);
+  static int min_deep = 0;  // units per warp with 4-stage rings (tuning knob FLEXQ_MIN_UNITS)
+  if (!min_deep) {
+    const char* e = getenv("FLEXQ_MIN_UNITS");
+    min_deep = (e && atoi(e) > 0) ? atoi(e) : 4;
+  }
+  const int64_t by_units = cdiv(p.units, S >= 4 ? min_deep : kMinUnitsPerWarp);
   if (warps > by_units) warps = by_units;
   p.nw = warps;
-  const unsigned ctas = (unsigned)cdiv(warps, kSWarps);
-  cudaError_t e = launch_pdl(kern, dim3(ctas), dim3(kSWarps * 32), (size_t)smem, st, p);
+  const unsigned ctas = (unsigned)cdiv(warps, wpc);
+  cudaError_t e = launch_pdl(kern, dim3(ctas), dim3(wpc * 32), (size_t)smem, st, p);
   if (e != cudaSuccess) return cuda_status(e, "gemv_t6_stream launch");
   return FLEXQ_OK;
 }

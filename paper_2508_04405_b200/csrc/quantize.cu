@@ -273,50 +273,61 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
   if (!A.early) pdl_launch_dependents();
   const long long dt1 = A.dbg ? dbg_now() : 0;
   const int lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int64_t ng = A.ng;
-  if (item >= A.rows * ng) return;
-  const int64_t r = item / ng, g = item - r * ng;  // once per warp
-  const __half* xr = reinterpret_cast<const __half*>(A.x) + r * A.cols + g * 128 + lane * 4;
-  const uint2 raw = *reinterpret_cast<const uint2*>(xr);
-  const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-  const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-  const double v[4] = {(double)f01.x, (double)f01.y, (double)f23.x, (double)f23.y};
-  bool finite = true;
-  float peak = 0.f;  // max of fp16 magnitudes: exact in fp32
+  const int64_t ng = A.ng, items = A.rows * ng;
+  // grid-stride over (row, group) items, two per pass with both loads issued first: the
+  // grid is capped at one CTA per SM so that the quantizer's CTAs never take the register
+  // room a persistent GEMM CTA launched behind it (PDL) needs on an SM
+  auto quantize_item = [&](int64_t item, uint2 raw) {
+    const int64_t r = item / ng, g = item - r * ng;
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+    const double v[4] = {(double)f01.x, (double)f01.y, (double)f23.x, (double)f23.y};
+    bool finite = true;
+    float peak = 0.f;  // max of fp16 magnitudes: exact in fp32
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    finite &= isfinite(v[i]);
-    peak = fmaxf(peak, fabsf((float)v[i]));
-  }
+    for (int i = 0; i < 4; i++) {
+      finite &= isfinite(v[i]);
+      peak = fmaxf(peak, fabsf((float)v[i]));
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
-  if (!__all_sync(0xffffffffu, finite)) {
-    if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
-    peak = 0.f;
-  }
-  const double sc = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
-  int c[4], csum = 0;
+    for (int o = 16; o; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    if (!__all_sync(0xffffffffu, finite)) {
+      if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
+      peak = 0.f;
+    }
+    const double sc = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
+    int c[4], csum = 0;
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    c[i] = code_of(v[i], sc, A.bits);
-    csum += c[i];
-  }
-  const uint32_t word = (uint32_t)(c[0] & 0xff) | ((uint32_t)(c[1] & 0xff) << 8) |
-                        ((uint32_t)(c[2] & 0xff) << 16) | ((uint32_t)(c[3] & 0xff) << 24);
-  if (A.codes) *reinterpret_cast<uint32_t*>(A.codes + r * A.cols + g * 128 + lane * 4) = word;
-  if (A.act_frag) {
-    const int jj = lane >> 3, h = (lane >> 2) & 1, t = lane & 3;
-    const int64_t off = ((g * (A.m_pad >> 3) + (r >> 3)) * 8 + 2 * t + h) * 128 + (r & 7) * 16 + jj * 4;
-    *reinterpret_cast<uint32_t*>(A.act_frag + off) = word;
-  }
+    for (int i = 0; i < 4; i++) {
+      c[i] = code_of(v[i], sc, A.bits);
+      csum += c[i];
+    }
+    const uint32_t word = (uint32_t)(c[0] & 0xff) | ((uint32_t)(c[1] & 0xff) << 8) |
+                          ((uint32_t)(c[2] & 0xff) << 16) | ((uint32_t)(c[3] & 0xff) << 24);
+    if (A.codes) *reinterpret_cast<uint32_t*>(A.codes + r * A.cols + g * 128 + lane * 4) = word;
+    if (A.act_frag)
+      *reinterpret_cast<uint32_t*>(A.act_frag + operand_word_offset(g, r, A.m_pad, lane)) = word;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
-  if (lane == 0) {
-    if (A.scales) A.scales[r * ng + g] = sc;
-    if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)sc;
-    if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
-    if (A.dbg) dbg_record(A.dbg, A.dbg_tag, dt0, dt1, dbg_now());
+    for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if (lane == 0) {
+      if (A.scales) A.scales[r * ng + g] = sc;
+      if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)sc;
+      if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
+      if (A.dbg) dbg_record(A.dbg, A.dbg_tag, dt0, dt1, dbg_now());
+    }
+  };
+  auto load = [&](int64_t item) {
+    const int64_t r = item / ng, g = item - r * ng;
+    return *reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(A.x) + r * A.cols +
+                                           g * 128 + lane * 4);
+  };
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t a = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); a < items; a += 2 * stride) {
+    const int64_t b = a + stride;
+    const uint2 ra = load(a);
+    const uint2 rb = b < items ? load(b) : make_uint2(0u, 0u);
+    quantize_item(a, ra);
+    if (b < items) quantize_item(b, rb);
   }
 }
 
@@ -327,7 +338,14 @@ static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
   const int64_t items = A.rows * A.ng;
   if (DT == FLEXQ_DT_F16 && A.gs == 128 && A.cols % 128 == 0 &&
       reinterpret_cast<uintptr_t>(A.x) % 8 == 0) {
-    launch_pdl(quantize_g128_kernel, dim3((unsigned)cdiv(items, 8)), dim3(256), 0, st, A);
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t ctas = cdiv(items, 8) < sms ? cdiv(items, 8) : sms;
+    launch_pdl(quantize_g128_kernel, dim3((unsigned)ctas), dim3(256), 0, st, A);
     return;
   }
   if (A.gs <= kWarpGroupMax || A.cols <= kWarpGroupMax) {

@@ -60,11 +60,14 @@ def main():
     n = fn(buf, cap)
     rec = np.frombuffer(buf, dtype=np.int64)[:4 * n].reshape(n, 4)
     t0 = rec[:, 1].min()
+    warp_of = rec[:, 0] >> 40  # GEMV records carry the warp index above bit 40
+    rec = rec.copy()
+    rec[:, 0] &= (1 << 40) - 1
     names = {1: "quantize", 2: "gemv", 3: "fused_quant", 4: "gemm_tc"}
     print(f"{model} M={m}: graph step {e0.elapsed_time(e1) * 1e3:.1f} us (events), "
           f"{(rec[:, 3].max() - t0) / 1e3:.1f} us first-start..last-end (globaltimer)")
     print(f"{'launch':>8} {'kind':>11} {'recs':>5} {'start0':>8} {'start50':>8} {'mid0':>8} "
-          f"{'mid50':>8} {'end50':>8} {'end100':>8} {'gap':>7}")
+          f"{'mid50':>8} {'end50':>8} {'end100':>8} {'gap':>7} {'late':>5}")
     prev_end = None
     for tag in sorted(set(rec[:, 0].tolist())):
         r = rec[rec[:, 0] == tag]
@@ -73,8 +76,10 @@ def main():
         gap = d[:, 0].min() - prev_end if prev_end is not None else 0.0
         print(f"{tag >> 8:>8} {kind:>11} {len(r):>5} {d[:, 0].min():8.2f} {np.median(d[:, 0]):8.2f} "
               f"{d[:, 1].min():8.2f} {np.median(d[:, 1]):8.2f} {np.median(d[:, 2]):8.2f} "
-              f"{d[:, 2].max():8.2f} {gap:7.2f}")
+              f"{d[:, 2].max():8.2f} {gap:7.2f} {int((d[:, 0] > d[:, 0].min() + 5).sum()):>5}")
         prev_end = d[:, 2].max()
+    np.save(os.path.join("gpurun_out", f"step_trace_{model}_m{m}.npy"),
+            np.hstack([rec, warp_of[:, None]]))
 
 
 if __name__ == "__main__":
