@@ -344,7 +344,9 @@ static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t ctas = cdiv(items, 8) < sms ? cdiv(items, 8) : sms;
+    // decode batches feed the persistent GEMV (3 CTAs per SM, registers nearly full): at most
+    // one quantizer CTA per SM.  Larger batches keep one warp per item (one wave).
+    const int64_t ctas = (A.rows <= 16 && cdiv(items, 8) > sms) ? sms : cdiv(items, 8);
     launch_pdl(quantize_g128_kernel, dim3((unsigned)ctas), dim3(256), 0, st, A);
     return;
   }
