@@ -122,7 +122,12 @@ int64_t flexq_gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int64_t grou
 
 /* Production path: unpack-to-INT8 + tensor cores over T6 weights.
  * Replaces int_matmul_reference / group_matmul_fused numerics (engine.py:290-365).
- * act_* are the fused outputs of flexq_quantize (same m_pad). */
+ * act_* are the fused outputs of flexq_quantize (same m_pad).
+ * ksplit: 0 = automatic kernel choice (streaming GEMV for M <= 32 with one group per
+ * 128-k block, M <= 16 otherwise; tcgen05 above), > 0 = the mma.sync kernel with that
+ * k-split, -1 = the mma.sync kernel (automatic split; GEMV for M <= 16), -2 = the tcgen05
+ * kernel whenever it supports the shape (M > 16), -3 = the streaming GEMV whenever it
+ * supports the shape (M <= 32). */
 int flexq_gemm_t6(const uint32_t* t6, const void* wscale, int scale_f16,
                   const uint32_t* act_frag, const float* act_scale, const int32_t* act_corr,
                   int64_t m, int64_t m_pad, int64_t n, int64_t k, int64_t group_size,

@@ -26,6 +26,7 @@
 // k-blocks (128 k-slots, 3 x LDG.128 per lane).  A warp's fp32 partial sums
 // are reduced across warps in fixed order, then across K-split CTAs by the
 // last-arriving CTA in fixed order -> deterministic output.
+#include <cstdint>
 #include "common.cuh"
 
 namespace flexq {
@@ -289,7 +290,7 @@ static int64_t ws_counters_offset(int64_t ksplit, int64_t m_pad, int64_t rt) {
   return cdiv(ksplit * mc * rt * kRowTile * 4, 256) * 256;
 }
 
-bool gemv_stream_supported(int64_t m, int64_t spg);
+bool gemv_stream_supported(int64_t m, int64_t spg, int64_t units);
 int64_t gemv_stream_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
 int gemv_stream_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
                        const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
@@ -323,7 +324,8 @@ int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int kspli
   const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
   const int64_t mc = m_pad < kT6TokChunk ? m_pad : kT6TokChunk;
   int64_t bytes = ws_counters_offset(ks_eff, mc, G.rt) + cdiv(G.rt * 4, 256) * 256;
-  if (ksplit <= 0 && gemv_stream_supported(m, G.spg)) {
+  if ((ksplit == -3 && gemv_stream_supported(m, G.spg, INT64_MAX)) ||
+      (ksplit <= 0 && (ksplit == 0 || m <= 16) && gemv_stream_supported(m, G.spg, G.rg * G.kb))) {
     const int64_t b2 = gemv_stream_workspace(m, n, k, gs);
     if (b2 > bytes) bytes = b2;
   }
@@ -331,7 +333,7 @@ int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int kspli
     const int64_t b4 = gemv_dyn_workspace(m, n, k, gs);
     if (b4 > bytes) bytes = b4;
   }
-  if (ksplit == 0 && gemm_tc_supported(m, tc_act_m_pad(m), G.spg)) {
+  if ((ksplit == 0 || ksplit == -2) && gemm_tc_supported(m, tc_act_m_pad(m), G.spg)) {
     const int64_t b3 = gemm_tc_workspace(m, n, k, gs);
     if (b3 > bytes) bytes = b3;
   }
@@ -363,12 +365,31 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
     return FLEXQ_ERR_CONFIG;
   }
   T6Geom G(n, k, gs);
+  // ksplit = -2: the tcgen05 kernel even where the streaming GEMV would be chosen (tests, A/B)
+  const bool force_tc = ksplit == -2;
+  if (force_tc) {
+    if (!gemm_tc_supported(m, m_pad, G.spg)) {
+      set_error("gemm_t6: ksplit=-2 (tcgen05) unsupported for m=%lld", (long long)m);
+      return FLEXQ_ERR_CONFIG;
+    }
+    return gemm_tc_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k, gs,
+                          partials, y, out_dtype, workspace, residual, st);
+  }
+  // ksplit = -3: the streaming GEMV whenever it supports the shape (tests, A/B)
+  if (ksplit == -3) {
+    if (!gemv_stream_supported(m, G.spg, INT64_MAX) || (fast && !workspace)) {
+      set_error("gemm_t6: ksplit=-3 (streaming GEMV) unsupported for m=%lld", (long long)m);
+      return FLEXQ_ERR_CONFIG;
+    }
+    return gemv_stream_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
+                              gs, partials, y, out_dtype, workspace, residual, st);
+  }
   // decode regime, one group per k-block: dynamically scheduled pieces (gemv_dyn.cu)
   if (ksplit == 0 && gemv_dyn_supported(m, G.spg) && workspace)
     return gemv_dyn_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
                            gs, partials, y, out_dtype, workspace, residual, st);
   // decode regime: the persistent TMA-fed streaming kernel (gemv_stream.cu)
-  if (ksplit <= 0 && gemv_stream_supported(m, G.spg) && (workspace || !fast))
+  if (ksplit <= 0 && (ksplit == 0 || m <= 16) && gemv_stream_supported(m, G.spg, G.rg * G.kb) && (workspace || !fast))
     return gemv_stream_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
                               gs, partials, y, out_dtype, workspace, residual, st);
   // batched regime: tcgen05.mma kind::i8 with TMEM accumulators (gemm_tc.cu)

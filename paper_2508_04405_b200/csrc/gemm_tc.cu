@@ -23,13 +23,12 @@
 //            registers, re-seed the TMEM buffer, flush the tile (direct fp16 store or a
 //            deterministic stream-K fixup through the workspace).
 //
-// The TMEM accumulator of every group starts at the integer 0x4B400000 instead of 0
-// (re-seeded by the epilogue with one tcgen05.st per 32 columns), so after the group
-// D = 0x4B400000 + sum u*x, which read as an fp32 is exactly 12582912 + sum u*x while
-// |sum u*x| < 2^22 (any group <= 512 elements; longer groups are drained every 512).
-// The dequant is then one FADD (which also removes the offset-binary correction),
-// one FMUL and one FFMA per element, and the exact integer is D - 0x4B400000.
-//
+// Every drain event's MMA chain starts from zero (enable-input-d off on its first K step), so
+// the buffer holds the group's integer partial P_u.  The epilogue reads it as the fp32 bits
+// 0x4B400000 + P_u, which is exactly 12582912 + P_u while |P_u| < 2^22 (any group <= 512
+// elements; longer groups are drained every 512), so the dequant is one IADD, one FADD (which
+// also removes the offset-binary correction), one FMUL and one FFMA per element, packed two
+// at a time (FADD2/FMUL2/FFMA2).
 // Work split (stream-K): units u = tile * KB + kb over (128-row x TN-token tiles,
 // k-blocks); CTA c owns units [c*U/P, (c+1)*U/P), so every CTA streams the same number
 // of weight bytes for every shape.  A tile split across CTAs is combined in CTA order
@@ -38,6 +37,10 @@
 
 #ifndef FLEXQ_EXP
 #define FLEXQ_EXP 0  // experiment bits for A/B profiling builds only (results invalid if set)
+#endif
+
+#ifndef FLEXQ_TC_REGACC_MAX
+#define FLEXQ_TC_REGACC_MAX 64  // token tiles up to this width keep the fp32 accumulator in registers
 #endif
 
 #include "common.cuh"
@@ -126,8 +129,8 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 
 constexpr int kTcRows = 128;                 // weight rows per tile (UMMA M)
 constexpr int kTcConvWarps = 4;              // warps 0-3: two 16-row tiles each per k-block
-constexpr int kTcWarpProdW = 4, kTcWarpMma = 5, kTcWarpProdB = 6, kTcWarpProdS = 7;
-constexpr int kTcWarpEpi0 = 8;               // epilogue: warps 8 .. 8 + kEpiWarps - 1
+constexpr int kTcWarpProdW = 4, kTcWarpMma = 5, kTcWarpProdB = 6;  // warp 6 also feeds the slots
+constexpr int kTcWarpEpi0 = 7;               // epilogue: warps 7 .. 7 + kEpiWarps - 1 (two per TMEM lane quarter)
 constexpr uint32_t kSeed = 0x4B400000u;      // fp32 bits of 12582912 = 1.5 * 2^23
 constexpr int kMaxDrainKb = 4;               // exact fp32 reinterpretation needs <= 512 k per drain
 
@@ -141,14 +144,14 @@ struct TcCfg {
   //    warp as soon as it is in registers (NB = 8 buffers in flight);
   //  * TN = 128: two event groups of 4 warps drain alternate events into their own fp32
   //    accumulators in TMEM (the register file cannot hold 64 columns per thread here);
-  //    the MMA accumulates onto a seeded buffer (kSeed) that the epilogue re-seeds.
-  static constexpr bool kRegAcc = TN <= 64;
+  //    each TMEM round trip moves 32 columns of partials and accumulators.
+  static constexpr bool kRegAcc = TN <= FLEXQ_TC_REGACC_MAX;
   static constexpr int kEpiWarps = 8;
   static constexpr int kThreads = (kTcWarpEpi0 + kEpiWarps) * 32;
   static constexpr int CH = TN / 2;
   static constexpr int G = kRegAcc ? 1 : 2;                // event groups (TMEM-acc design)
   static constexpr int kDrainArrivals = kRegAcc ? 8 : 4;   // warps releasing one buffer
-  static constexpr int NB = kRegAcc ? 8 : 2;               // TMEM drain buffers
+  static constexpr int NB = kRegAcc ? 512 / TN < 8 ? 512 / TN : 8 : 2;  // TMEM drain buffers
   // kRegAcc: the MMA and epilogue warps hand TMEM buffers over in pairs of consecutive drain
   // events (one dfull commit / dempty wait per two groups), halving the synchronisation per
   // k-block on both sides; EV = drain events per hand-over, NE = hand-over barriers
@@ -255,29 +258,6 @@ struct TcCursor {
   }
 };
 
-// packed fp32x2 math (FADD2 / FMUL2 / FFMA2 on sm_100)
-__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
-      "sub.rn.f32x2 rd, ra, rb;\nmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
-      "mul.rn.f32x2 rd, ra, rb;\nmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
-      "mov.b64 rc, {%6,%7};\nfma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -412,12 +392,15 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       }
     }
   } else if (warp == kTcWarpProdB) {
-    // ===== activation producer: B tiles (L2-resident, SB deep ahead of the MMA) =====
+    // ===== activation producer: B tiles (L2-resident, SA deep ahead of the MMA) and, per
+    // drain event, the slot of xs / corr of the token tile and the weight scales of the 128
+    // rows (SS events ahead of the epilogue); one loop (measured as fast as two warps) =====
     if (lane == 0) {
       pdl_wait();
       const uint64_t pol = l2_policy_evict_last();
-      int bi = 0;
-      uint32_t bph = 0;
+      constexpr uint32_t swb = 4 * 8 * 2 * (SF16 ? 2 : 4);  // one row group's scales of a group
+      int bi = 0, si = 0;
+      uint32_t bph = 0, sph = 0;
       for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
         mbar_wait(&aempty[bi], bph ^ 1u);
         mbar_expect_tx(&afull[bi], C::kB);
@@ -425,18 +408,6 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
                  p.act + ((int64_t)c.kb * (p.m_pad >> 3) + (int64_t)c.tt * (TN / 8)) * 1024, C::kB,
                  &afull[bi], pol);
         if (++bi == C::SA) { bi = 0; bph ^= 1u; }
-      }
-    }
-  } else if (warp == kTcWarpProdS) {
-    // ===== slot producer: per drain event, xs / corr of the token tile and the weight
-    // scales of the 128 rows (SS events ahead of the epilogue) =====
-    if (lane == 0) {
-      pdl_wait();
-      const uint64_t pol = l2_policy_evict_last();
-      constexpr uint32_t swb = 4 * 8 * 2 * (SF16 ? 2 : 4);  // one row group's scales of a group
-      int si = 0;
-      uint32_t sph = 0;
-      for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
         if (!c.drain_end(p)) continue;
         mbar_wait(&sempty[si], sph ^ 1u);
         const int rg0 = c.rt * 2;
@@ -478,7 +449,7 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
 #pragma unroll
         for (int s = 0; s < 4; s++)  // K=32 step s: A +32 B (swizzled rows), B +256 B (2 cores)
           tc_mma_i8(tmem + b * TN, ad + (uint64_t)(s * 2), bd + (uint64_t)(s * 16), C::kIdesc,
-                    (C::kRegAcc && ev_first && s == 0) ? 0u : 1u);
+                    (ev_first && s == 0) ? 0u : 1u);
         tl_mark(p, 1, c.u - u0, 2);
         tc_commit(&aempty[ai]);
         tl_mark(p, 1, c.u - u0, 3);
@@ -647,11 +618,14 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
             for (int64_t cc = first_c; cc <= last_c; cc++) {  // fixed CTA order: deterministic
               const int wc = tc_unit_start(cc, U, P) >= tile * kbn ? 0 : 1;
               const float* src = p.ws_part + ((cc * 2 + wc) * TN + hc * CH) * (int64_t)kTcRows + rho;
-              float v[CH];
 #pragma unroll
-              for (int j = 0; j < CH; j++) v[j] = __ldcg(src + j * kTcRows);
+              for (int j0 = 0; j0 < CH; j0 += 16) {  // 16 loads in flight per L2 round trip
+                float v[16];
 #pragma unroll
-              for (int j = 0; j < CH; j++) acc[j] += v[j];
+                for (int j = 0; j < 16; j++) v[j] = __ldcg(src + (j0 + j) * kTcRows);
+#pragma unroll
+                for (int j = 0; j < 16; j++) acc[j0 + j] += v[j];
+              }
             }
             store_row(tt, n_row, acc);
             if (e == 0 && lane == 0) p.counters[tile] = 0u;
@@ -673,9 +647,6 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
     const uint32_t tacc0 = tl + C::NB * TN;                  // accumulator of group 0
     const uint32_t tacc = tacc0 + gi * TN;                   // this group's accumulator
     const int rho = 32 * q + lane;  // tile row of this thread
-    for (int b = gi; b < C::NB; b += G)
-#pragma unroll
-      for (int c0 = 0; c0 < TN; c0 += 16) tmem_fill16(tl + b * TN + c0, kSeed);
 #pragma unroll
     for (int c0 = 0; c0 < TN; c0 += 16) tmem_fill16(tacc + c0, 0u);
     tmem_wait_st();
@@ -752,59 +723,56 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
           else sw = *reinterpret_cast<const float*>(slot + sw_off);
           const float2 sw2 = make_float2(sw, sw);
 #pragma unroll 1
-          for (int c0 = 0; c0 < TN; c0 += 16) {
-            // column table first (plain loads), then the TMEM round trip
-            float4 sv[4], cv[4];
-            if (p.dbg & 1) {
-#pragma unroll
-              for (int j = 0; j < 4; j++) { sv[j] = make_float4(sw, sw, sw, sw); cv[j] = sv[j]; }
-            } else {
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-              sv[j] = *reinterpret_cast<const float4*>(sx + c0 + 4 * j);
-              cv[j] = *reinterpret_cast<const float4*>(cvp + c0 + 4 * j);
-            }
-            }
-            if (cmode == 2) {
-#pragma unroll
-              for (int j = 0; j < 4; j++) {
-                const int4 c4 = *reinterpret_cast<const int4*>(cr + c0 + 4 * j);
-                cv[j] = make_float4(12582912.f + (float)(c4.x - kCorrBias), 12582912.f + (float)(c4.y - kCorrBias),
-                                    12582912.f + (float)(c4.z - kCorrBias), 12582912.f + (float)(c4.w - kCorrBias));
-              }
-            }
-            if (e == 0 && lane == 0 && c0 == 0) tl_mark(p, 2, c.u - u0, 1);
-            uint32_t v[16], av[16];
-            tmem_ld16x(tl + b * TN + c0, v);
-            tmem_ld16x(tacc + c0, av);
-            tmem_wait_ld_r2(v, av);
+          for (int c0 = 0; c0 < TN; c0 += 32) {
+            // one TMEM round trip per 32 columns: partials (the MMA started the group from
+            // zero) and this group's accumulator, then the column table from shared memory
+            uint32_t v[2][16], av[2][16];
+            tmem_ld16x(tl + b * TN + c0, v[0]);
+            tmem_ld16x(tacc + c0, av[0]);
+            tmem_ld16x(tl + b * TN + c0 + 16, v[1]);
+            tmem_ld16x(tacc + c0 + 16, av[1]);
+            tmem_wait_ld_r2(v[0], av[0]);
+            tmem_wait_ld_r2(v[1], av[1]);  // (already complete: pins the second half's uses)
             if (e == 0 && lane == 0 && c0 == 0) tl_mark(p, 2, c.u - u0, 2);
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-              const float2 s01 = f2_mul(sw2, make_float2(sv[j].x, sv[j].y));
-              const float2 s23 = f2_mul(sw2, make_float2(sv[j].z, sv[j].w));
-              const float2 f01 = f2_sub(make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1])),
-                                        make_float2(cv[j].x, cv[j].y));
-              const float2 f23 = f2_sub(make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])),
-                                        make_float2(cv[j].z, cv[j].w));
-              const float2 a01 = f2_fma(s01, f01, make_float2(__uint_as_float(av[4 * j]), __uint_as_float(av[4 * j + 1])));
-              const float2 a23 = f2_fma(s23, f23, make_float2(__uint_as_float(av[4 * j + 2]), __uint_as_float(av[4 * j + 3])));
-              av[4 * j] = __float_as_uint(a01.x); av[4 * j + 1] = __float_as_uint(a01.y);
-              av[4 * j + 2] = __float_as_uint(a23.x); av[4 * j + 3] = __float_as_uint(a23.y);
-            }
-            tmem_st16(tacc + c0, av);
-            if constexpr (TRACE) {
+            for (int h = 0; h < 2; h++) {
+              const int cc = c0 + 16 * h;
 #pragma unroll
-              for (int j = 0; j < 16; j++) {
-                const int64_t m = tt * TN + c0 + j;
-                if (m < p.m && n_row < p.n) {
-                  const int P = (int)(v[j] - kSeed) - (first ? cr[c0 + j] - kCorrBias : 0);
-                  atomicAdd(&p.partials[((int64_t)c.g * p.m + m) * p.n + n_row], P);
+              for (int j = 0; j < 4; j++) {
+                const float4 sv = *reinterpret_cast<const float4*>(sx + cc + 4 * j);
+                float4 cv;
+                if (cmode == 2) {
+                  const int4 c4 = *reinterpret_cast<const int4*>(cr + cc + 4 * j);
+                  cv = make_float4(12582912.f + (float)(c4.x - kCorrBias), 12582912.f + (float)(c4.y - kCorrBias),
+                                   12582912.f + (float)(c4.z - kCorrBias), 12582912.f + (float)(c4.w - kCorrBias));
+                } else {
+                  cv = *reinterpret_cast<const float4*>(cvp + cc + 4 * j);
+                }
+                const float2 s01 = f2_mul(sw2, make_float2(sv.x, sv.y));
+                const float2 s23 = f2_mul(sw2, make_float2(sv.z, sv.w));
+                const uint32_t* vv = &v[h][4 * j];
+                uint32_t* aa = &av[h][4 * j];
+                const float2 f01 = f2_sub(make_float2(__uint_as_float(vv[0] + kSeed), __uint_as_float(vv[1] + kSeed)),
+                                          make_float2(cv.x, cv.y));
+                const float2 f23 = f2_sub(make_float2(__uint_as_float(vv[2] + kSeed), __uint_as_float(vv[3] + kSeed)),
+                                          make_float2(cv.z, cv.w));
+                const float2 a01 = f2_fma(s01, f01, make_float2(__uint_as_float(aa[0]), __uint_as_float(aa[1])));
+                const float2 a23 = f2_fma(s23, f23, make_float2(__uint_as_float(aa[2]), __uint_as_float(aa[3])));
+                aa[0] = __float_as_uint(a01.x); aa[1] = __float_as_uint(a01.y);
+                aa[2] = __float_as_uint(a23.x); aa[3] = __float_as_uint(a23.y);
+              }
+              tmem_st16(tacc + cc, av[h]);
+              if constexpr (TRACE) {
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                  const int64_t m = tt * TN + cc + j;
+                  if (m < p.m && n_row < p.n) {
+                    const int P = (int)v[h][j] - (first ? cr[cc + j] - kCorrBias : 0);
+                    atomicAdd(&p.partials[((int64_t)c.g * p.m + m) * p.n + n_row], P);
+                  }
                 }
               }
             }
-            tmem_fill16(tl + b * TN + c0, kSeed);  // re-seed for the buffer's next group
-            if (e == 0 && lane == 0 && c0 == 0) tl_mark(p, 2, c.u - u0, 3);
           }
         } else {  // trace only
 #pragma unroll 1
@@ -816,11 +784,10 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
             for (int j = 0; j < 16; j++) {
               const int64_t m = tt * TN + c0 + j;
               if (m < p.m && n_row < p.n) {
-                const int P = (int)(v[j] - kSeed) - (first ? cr[c0 + j] - kCorrBias : 0);
+                const int P = (int)v[j] - (first ? cr[c0 + j] - kCorrBias : 0);
                 atomicAdd(&p.partials[((int64_t)c.g * p.m + m) * p.n + n_row], P);
               }
             }
-            tmem_fill16(tl + b * TN + c0, kSeed);
           }
         }
         tmem_wait_st();

@@ -34,7 +34,9 @@ namespace flexq {
 constexpr int kSWarps = 4;  // warps per CTA in the default launch (independent pipelines)
 // Warps per CTA are a launch parameter (blockDim): the default packs 4-warp CTAs several to
 // an SM; FLEXQ_GEMV_WIDE=1 launches one CTA per SM holding all of that SM's warps.
-constexpr int kMaxWarpsMT1 = 12, kMaxWarpsMT2 = 8;
+constexpr int kMaxWarpsMT1 = 12, kMaxWarpsMT2 = 8, kMaxWarpsMT4 = 8;
+template <int MT>
+constexpr int max_warps() { return MT == 1 ? kMaxWarpsMT1 : MT == 2 ? kMaxWarpsMT2 : kMaxWarpsMT4; }
 constexpr int kMinUnitsPerWarp = 6;
 #ifndef FLEXQ_GEMV_FB1
 #define FLEXQ_GEMV_FB1 8  // split-fixup slots loaded per L2 round trip at M = 1
@@ -71,7 +73,7 @@ template <int MT, int MODE, bool SF16>
 struct StageLayout {
   static constexpr int kNgr = MODE == 1 ? 4 : 1;
   static constexpr int kWs = kNgr * kRowGroup * 8 * (SF16 ? 4 : 8);
-  static constexpr int kVec = kNgr * 16 * 4;  // m_pad <= 16 tokens x 4 B
+  static constexpr int kVec = kNgr * (MT <= 2 ? 16 : 8 * MT) * 4;  // m_pad tokens x 4 B
   static constexpr int kOffB = kUnitBytes;
   static constexpr int kOffWs = kOffB + MT * 1024;
   static constexpr int kOffXs = kOffWs + kWs;
@@ -97,9 +99,11 @@ __device__ __forceinline__ void store_out(void* y, int64_t i, float v) {
 // ONE: m == 1 (decode GEMV) -- only accumulator column 0 (c0, c2) is live, so the
 // dequant, the split fixup and the stores touch half the values.
 template <int MT, int MODE, bool SF16, bool TRACE, bool FAST, int OUT, int S, bool ONE>
-__global__ void __launch_bounds__((MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2) * 32, 1)
+__global__ void __launch_bounds__(max_warps<MT>() * 32, 1)
     gemv_t6_stream_kernel(StreamParams p) {
   static_assert(!ONE || MT == 1, "ONE implies a single token tile");
+  constexpr bool ROUT = MT >= 4;  // row-tile-outer unit loop (M <= 32, MODE 0 only)
+  static_assert(!ROUT || MODE == 0, "MT = 4 needs one group per k-block");
   using L = StageLayout<MT, MODE, SF16>;
   constexpr int UB = L::kBytes;
   constexpr int SB = SF16 ? 4 : 8;  // bytes of one weight-scale pair
@@ -254,7 +258,32 @@ __global__ void __launch_bounds__((MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2) * 32, 
               atomicAdd(&p.partials[(g * p.m + tok) * p.n + row], P[r][mt][i]);
           }
       }
-      if constexpr (FAST) {
+      if constexpr (FAST && MODE != 2) {
+        // |P| < 2^22 for groups <= 128: convert without I2F (0x4B400000 + P read as an fp32 is
+        // 12582912 + P exactly) and dequantise with packed FADD2/FMUL2/FFMA2 -- the same
+        // IEEE operations as fmaf(sw * sx, (float)P, acc)
+        const float2 c2 = make_float2(12582912.f, 12582912.f);
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          if (ONE) {
+            const float2 f = f2_sub(make_float2(__int_as_float(P[r][mt][0] + kCorrBias),
+                                                __int_as_float(P[r][mt][2] + kCorrBias)), c2);
+            const float2 sc = f2_mul(sw[r], make_float2(sx[mt].x, sx[mt].x));
+            const float2 a = f2_fma(sc, f, make_float2(acc[r][mt][0], acc[r][mt][2]));
+            acc[r][mt][0] = a.x; acc[r][mt][2] = a.y;
+          } else {
+            const float2 f01 = f2_sub(make_float2(__int_as_float(P[r][mt][0] + kCorrBias),
+                                                  __int_as_float(P[r][mt][1] + kCorrBias)), c2);
+            const float2 f23 = f2_sub(make_float2(__int_as_float(P[r][mt][2] + kCorrBias),
+                                                  __int_as_float(P[r][mt][3] + kCorrBias)), c2);
+            const float2 s01 = f2_mul(make_float2(sw[r].x, sw[r].x), sx[mt]);
+            const float2 s23 = f2_mul(make_float2(sw[r].y, sw[r].y), sx[mt]);
+            const float2 a01 = f2_fma(s01, f01, make_float2(acc[r][mt][0], acc[r][mt][1]));
+            const float2 a23 = f2_fma(s23, f23, make_float2(acc[r][mt][2], acc[r][mt][3]));
+            acc[r][mt][0] = a01.x; acc[r][mt][1] = a01.y; acc[r][mt][2] = a23.x; acc[r][mt][3] = a23.y;
+          }
+        }
+      } else if constexpr (FAST) {
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) {
           acc[r][mt][0] = fmaf(sw[r].x * sx[mt].x, (float)P[r][mt][0], acc[r][mt][0]);
@@ -306,7 +335,7 @@ __global__ void __launch_bounds__((MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2) * 32, 
 #pragma unroll
           for (int i = 0; i < 4; i++) acc[r][mt][i] = 0.f;
       // fixed order; FB contributors' slots in flight per L2 round trip
-      constexpr int FB = ONE ? FLEXQ_GEMV_FB1 : (MT == 1 ? 4 : 2);  // measured best (tools/sweep.py)
+      constexpr int FB = ONE ? FLEXQ_GEMV_FB1 : (MT == 1 ? 4 : MT == 2 ? 2 : 1);  // measured best (tools/sweep.py)
       for (int64_t w = first; w <= last; w += FB) {
         float v[FB][4][MT][4];
 #pragma unroll
@@ -358,6 +387,63 @@ __global__ void __launch_bounds__((MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2) * 32, 
     if (p.tl && lane == 0 && u == u0) p.tl[gw * 8 + 4] = gv_timer();
     if (p.dbg && u == u0) dt1 = dbg_now();
     const uint8_t* st = ring + s * UB;
+    if constexpr (ROUT) {
+      // MT = 4 (M <= 32), one group per k-block: row tile outermost, so only one row
+      // tile's weights and INT32 partials are live (MT independent mma chains per k-step)
+      uint4 bv[MT][2];
+      int2 cz[MT], cb[MT];  // corrections; cb = 0x4B400000 - corr (the fp32 conversion bias)
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        bv[mt][0] = lds128(st + L::kOffB + mt * 1024 + (2 * t) * 128 + gq * 16);
+        bv[mt][1] = lds128(st + L::kOffB + mt * 1024 + (2 * t + 1) * 128 + gq * 16);
+        cz[mt] = reinterpret_cast<const int2*>(st + L::kOffCorr)[(mt * kTokTile) / 2 + t];
+        cz[mt].x -= kCorrBias; cz[mt].y -= kCorrBias;
+        cb[mt] = make_int2(kCorrBias - cz[mt].x, kCorrBias - cz[mt].y);
+      }
+      float2 sw[4], sx[MT];
+      if constexpr (FAST) stage_scales(st, 0, sw, sx);
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const uint4 w0 = lds128(st + (r * 3 + 0) * 512 + lane * 16);
+        const uint4 w1 = lds128(st + (r * 3 + 1) * 512 + lane * 16);
+        const uint4 w2 = lds128(st + (r * 3 + 2) * 512 + lane * 16);
+        int Pr[MT][4];
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          uint32_t a[4];
+          unpack_t6(u4get(w0, jj), u4get(w1, jj), u4get(w2, jj), a);
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++) {
+            if (jj == 0) mma_u8s8_zc(Pr[mt], a, bv[mt][0].x, bv[mt][1].x);
+            else mma_u8s8(Pr[mt], a, u4get(bv[mt][0], jj), u4get(bv[mt][1], jj));
+          }
+        }
+        const int64_t row0 = ((int64_t)rg * kRowGroup + r) * kRowTile + gq, row1 = row0 + 8;
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          if constexpr (TRACE) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              const int64_t tok = mt * kTokTile + 2 * t + (i & 1), row = (i & 2) ? row1 : row0;
+              if (tok < p.m && row < p.n)
+                atomicAdd(&p.partials[((int64_t)kb * p.m + tok) * p.n + row], Pr[mt][i] - (i & 1 ? cz[mt].y : cz[mt].x));
+            }
+          }
+          if constexpr (FAST) {
+            // P = Pr - corr (|P| < 2^22 for a 128-k group) as an fp32 without I2F: the bits
+            // 0x4B400000 + P read as 12582912 + P, exactly; packed FADD2/FMUL2/FFMA2
+            const float2 c2 = make_float2(12582912.f, 12582912.f);
+            const float2 f01 = f2_sub(make_float2(__int_as_float(Pr[mt][0] + cb[mt].x), __int_as_float(Pr[mt][1] + cb[mt].y)), c2);
+            const float2 f23 = f2_sub(make_float2(__int_as_float(Pr[mt][2] + cb[mt].x), __int_as_float(Pr[mt][3] + cb[mt].y)), c2);
+            const float2 s01 = f2_mul(make_float2(sw[r].x, sw[r].x), sx[mt]);
+            const float2 s23 = f2_mul(make_float2(sw[r].y, sw[r].y), sx[mt]);
+            const float2 a01 = f2_fma(s01, f01, make_float2(acc[r][mt][0], acc[r][mt][1]));
+            const float2 a23 = f2_fma(s23, f23, make_float2(acc[r][mt][2], acc[r][mt][3]));
+            acc[r][mt][0] = a01.x; acc[r][mt][1] = a01.y; acc[r][mt][2] = a23.x; acc[r][mt][3] = a23.y;
+          }
+        }
+      }
+    } else {
     uint4 bv[MT][2], w[4][3];
 #pragma unroll
     for (int mt = 0; mt < MT; mt++) {
@@ -411,6 +497,7 @@ __global__ void __launch_bounds__((MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2) * 32, 
         }
       }
     }
+    }  // !ROUT
     __syncwarp();
     if (lane == 0 && iu < u1) {
       fence_proxy_async_smem();
@@ -477,7 +564,24 @@ extern "C" int flexq_debug_gemv_timeline(long long* host, int max_entries) {
   return n;
 }
 
-bool gemv_stream_supported(int64_t m, int64_t spg) { return m <= 16 && stream_mode(spg) >= 0; }
+// M <= 16 for every group layout; 16 < M <= 32 (MT = 4) for one group per k-block, where the
+// mma.sync stream beats the tcgen05 kernel (FLEXQ_STREAM_MAX_M = 16 turns it off)
+static int64_t stream_max_m() {
+  static int64_t v = 0;
+  if (!v) {
+    const char* e = getenv("FLEXQ_STREAM_MAX_M");
+    v = (e && atoi(e) >= 1) ? atoi(e) : 32;
+  }
+  return v;
+}
+// M in (16, 32] only for layers of >= 8192 units (48 MB of T6 weights): smaller layers have
+// too few units per warp to hide the MT = 4 split fixup, and tcgen05 is faster there
+// (LLaMA-2-7B shapes, tools/sweep.py r01)
+bool gemv_stream_supported(int64_t m, int64_t spg, int64_t units) {
+  if (m > stream_max_m()) return false;
+  if (m <= 16) return stream_mode(spg) >= 0;
+  return m <= 32 && stream_mode(spg) == 0 && units >= 8192;
+}
 
 static int stream_stages() {
   static int s = 0;
@@ -494,7 +598,7 @@ static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
   auto kern = (MT == 1 && p.m == 1) ? gemv_t6_stream_kernel<MT, MODE, SF16, TRACE, FAST, OUT, S, MT == 1>
                                     : gemv_t6_stream_kernel<MT, MODE, SF16, TRACE, FAST, OUT, S, false>;
   constexpr int UB = StageLayout<MT, MODE, SF16>::kBytes;
-  constexpr int kMaxW = MT == 1 ? kMaxWarpsMT1 : kMaxWarpsMT2;
+  constexpr int kMaxW = max_warps<MT>();
   static const bool wide = getenv("FLEXQ_GEMV_WIDE") != nullptr;
   static bool configured[2] = {false, false};  // one attribute call per instantiation
   const int ci = (MT == 1 && p.m == 1) ? 1 : 0;
@@ -558,7 +662,7 @@ static int64_t stream_slots(int64_t rg) { return rg + 148 * 16 + 16; }
 
 int64_t gemv_stream_workspace(int64_t m, int64_t n, int64_t k, int64_t gs) {
   T6Geom G(n, k, gs);
-  const int64_t mt = m <= 8 ? 1 : 2;
+  const int64_t mt = m <= 8 ? 1 : m <= 16 ? 2 : 4;
   return cdiv(stream_slots(G.rg) * 4 * mt * 4 * 32 * 4, 256) * 256 + cdiv(G.rg * 4, 256) * 256;
 }
 
@@ -568,7 +672,7 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
                        int out_dtype, void* workspace, const void* residual, cudaStream_t st) {
   T6Geom G(n, k, gs);
   const int mode = stream_mode(G.spg);
-  if (m > 16 || mode < 0) {
+  if (m > 32 || mode < 0 || (m > 16 && mode != 0)) {  // (the unit threshold is a routing choice)
     set_error("gemv_stream: unsupported m=%lld / group_size=%lld", (long long)m, (long long)gs);
     return FLEXQ_ERR_CONFIG;
   }
@@ -605,7 +709,7 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
     p.tl = tlbuf;
     g_gemv_tl = tlbuf;
   }
-  const int mt = m <= 8 ? 1 : 2;
+  const int mt = m <= 8 ? 1 : m <= 16 ? 2 : 4;
   if (workspace) {
     p.ws_part = reinterpret_cast<float*>(workspace);
     p.counters = reinterpret_cast<unsigned*>(
@@ -618,7 +722,8 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   const int forced = stream_stages();
   // ring depth by layer size (measured on B200, tools/sweep.py): small layers are latency-
   // bound and want every unit of a warp in flight; large ones want more warps per SM
-  const int S = forced > 0 ? forced : (p.units <= 4096 ? 4 : p.units <= 12288 ? 3 : 2);
+  // MT = 4 stages are 10.6 KB: two per warp keep 8 warps (two CTAs) per SM in shared memory
+  const int S = forced > 0 ? forced : mt == 4 ? 2 : (p.units <= 4096 ? 4 : p.units <= 12288 ? 3 : 2);
 #define FLEXQ_SM(MT_, MODE_, S_)                                                          \
   if (mt == MT_ && mode == MODE_ && S == S_)                                              \
     return dispatch_stream_flags<MT_, MODE_, S_>(p, sf16, trace, fast, out_dtype, sms, st);
@@ -626,6 +731,7 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   FLEXQ_SM(2, 0, 2) FLEXQ_SM(2, 1, 2) FLEXQ_SM(2, 2, 2)
   FLEXQ_SM(1, 0, 3) FLEXQ_SM(2, 0, 3)
   FLEXQ_SM(1, 0, 4) FLEXQ_SM(2, 0, 4)
+  FLEXQ_SM(4, 0, 2) FLEXQ_SM(4, 0, 3) FLEXQ_SM(4, 0, 4)
 #undef FLEXQ_SM
   if (S >= 3) {  // only MODE 0 has 3/4-stage instances; others use 2
 #define FLEXQ_SM2(MT_, MODE_)                                                             \

@@ -293,7 +293,7 @@ def _fast_case(m, n, k, q, gs, seed=0, outlier=True):
     return w, x, (wc, wsc, xc, xsc), y_ref, p_ref
 
 
-def _run_t6(codes, m, n, k, gs, trace=True):
+def _run_t6(codes, m, n, k, gs, trace=True, ksplit=0):
     wc, wsc, xc, xsc = codes
     L = _lib.lib()
     t6, wsp = t6_pack_weights(torch.from_numpy(wc).cuda(), torch.from_numpy(wsc).cuda(), k, gs, True)
@@ -302,10 +302,11 @@ def _run_t6(codes, m, n, k, gs, trace=True):
     ng = -(-k // gs)
     parts = torch.zeros((ng, m, n), dtype=torch.int32, device="cuda") if trace else None
     y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-    ws = torch.zeros(L.flexq_gemm_workspace_bytes(m, n, k, gs, 0), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(L.flexq_gemm_workspace_bytes(m, n, k, gs, ksplit), dtype=torch.uint8,
+                     device="cuda")
     _lib.check(L.flexq_gemm_t6(_lib.ptr(t6), _lib.ptr(wsp), 1, _lib.ptr(frag), _lib.ptr(xs),
                                _lib.ptr(corr), m, m_pad, n, k, gs, _lib.ptr(parts), _lib.ptr(y),
-                               _lib.OUT_F16, _lib.ptr(ws), 0, _lib.stream()))
+                               _lib.OUT_F16, _lib.ptr(ws), ksplit, _lib.stream()))
     torch.cuda.synchronize()
     return y.float().cpu().numpy(), (parts.cpu().numpy() if trace else None)
 
@@ -314,6 +315,7 @@ LLAMA = [  # (m, n, k, q): LLaMA-2 7B/13B/70B linear shapes
     (1, 4096, 4096, 8), (8, 11008, 4096, 6), (4, 4096, 11008, 8), (1, 15360, 5120, 6),
     (8, 5120, 13824, 8), (1, 10240, 8192, 6), (2, 28672, 8192, 6), (1, 8192, 28672, 8),
     (8, 8192, 28672, 8), (16, 8192, 8192, 6),
+    (32, 28672, 8192, 6), (24, 8192, 28672, 8), (17, 4096, 11008, 8),  # streaming GEMV, MT = 4
 ]
 
 
@@ -330,15 +332,17 @@ def test_t6_fast_path_llama_shapes(m, n, k, q):
     (1, 1000, 1024, 6, 32), (3, 200, 1024, 8, 64), (5, 256, 2048, 6, 256), (2, 512, 4096, 8, 4096),
     (16, 384, 896, 6, 128), (12, 130, 640, 8, 100), (9, 1024, 1536, 6, 512), (1, 64, 128, 6, 128),
     (20, 96, 1024, 8, 128), (64, 128, 512, 6, 128), (100, 72, 384, 8, 128), (1, 8, 300, 6, 128),
+    (25, 136, 1024, 6, 128), (32, 8, 300, 8, 128), (31, 1000, 4096, 6, 128),  # MT = 4 stream
 ])
 def test_t6_group_sizes_and_batches(m, n, k, q, gs):
     _, _, codes, y_ref, p_ref = _fast_case(m, n, k, q, gs, seed=gs + m)
-    y, parts = _run_t6(codes, m, n, k, gs)
+    # 16 < M <= 32 at group 128: force the streaming GEMV (automatic only for large layers)
+    y, parts = _run_t6(codes, m, n, k, gs, ksplit=-3 if 16 < m <= 32 and gs == 128 else 0)
     assert np.array_equal(parts, p_ref)
     assert max_rel(y, y_ref) <= FP16_TOL
 
 
-@pytest.mark.parametrize("m", [1, 4, 8, 13, 16, 33])
+@pytest.mark.parametrize("m", [1, 4, 8, 13, 16, 28, 33])
 def test_flexq_linear_public_api(m):
     """FlexQLinear (fused quantizer + GEMM from fp16 x) vs the oracle on fp16 inputs."""
     n, k = 2048, 4096

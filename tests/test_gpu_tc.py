@@ -21,7 +21,9 @@ from paper_2508_04405_b200 import _lib  # noqa: E402
 from paper_2508_04405_b200.engine import t6_pack_activations, t6_pack_weights  # noqa: E402
 
 FP16_TOL = 1e-3
-AUTO, LEGACY = 0, -1  # ksplit: 0 = auto (tcgen05 for M > 16), -1 = the mma.sync kernel
+# ksplit: 0 = auto (streaming GEMV up to M = 32 at group 128, tcgen05 above), -1 = the
+# mma.sync kernel, -2 = tcgen05 whenever it supports the shape (M > 16)
+AUTO, LEGACY, TC, STREAM = 0, -1, -2, -3
 
 
 def max_rel(y, ref):
@@ -39,7 +41,7 @@ def case(m, n, k, q, gs, seed):
     return w, x, (wc, wsc, xc, xsc), y_ref, p_ref
 
 
-def run(codes, m, n, k, gs, ksplit=AUTO, trace=True, fast=True):
+def run(codes, m, n, k, gs, ksplit=TC, trace=True, fast=True):
     wc, wsc, xc, xsc = codes
     L = _lib.lib()
     t6, wsp = t6_pack_weights(torch.from_numpy(wc).cuda(), torch.from_numpy(wsc).cuda(), k, gs, True)
@@ -97,10 +99,22 @@ def test_tc_llama13b_shapes(m, n, k, q):
 def test_tc_matches_mma_sync_kernel():
     m, n, k, q, gs = 80, 768, 3072, 8, 128
     _, _, codes, y_ref, p_ref = case(m, n, k, q, gs, seed=3)
-    y_tc, p_tc = run(codes, m, n, k, gs, AUTO)
+    y_tc, p_tc = run(codes, m, n, k, gs, TC)
     y_ms, p_ms = run(codes, m, n, k, gs, LEGACY)
     assert np.array_equal(p_tc, p_ref) and np.array_equal(p_ms, p_ref)
     assert max_rel(y_tc, y_ref) <= FP16_TOL and max_rel(y_ms, y_ref) <= FP16_TOL
+
+
+@pytest.mark.parametrize("m", [17, 32])
+def test_stream_and_tc_agree_at_small_batches(m):
+    """M in (16, 32] at group 128: the streaming GEMV (MT = 4; automatic for layers of >= 8192
+    units) and the tcgen05 kernel give identical INT32 partials and fp16 outputs in tolerance."""
+    n, k, gs = 640, 2048, 128
+    _, _, codes, y_ref, p_ref = case(m, n, k, 8, gs, seed=11 * m)
+    y_a, p_a = run(codes, m, n, k, gs, STREAM)
+    y_t, p_t = run(codes, m, n, k, gs, TC)
+    assert np.array_equal(p_a, p_ref) and np.array_equal(p_t, p_ref)
+    assert max_rel(y_a, y_ref) <= FP16_TOL and max_rel(y_t, y_ref) <= FP16_TOL
 
 
 @pytest.mark.parametrize("m", [24, 100, 256])

@@ -22,6 +22,10 @@ __device__ __forceinline__ void wait(uint64_t* bar, uint32_t ph) {
   asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@!P1 bra W;\n}\n" ::"r"(s32(bar)), "r"(ph), "r"(0x989680) : "memory");
 }
 
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(a), "l"(b), "r"(idesc) : "memory");
+}
+
 template <int N>
 __global__ void probe(long long* out, int iters, int mode) {
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -57,8 +61,20 @@ __global__ void probe(long long* out, int iters, int mode) {
       const int st = it & 3;
       const uint64_t ad = (mode & 1) ? desc_sw128(s32(A + st * 16384)) : desc_none(s32(A + st * 16384));
       const uint64_t bd = desc_none(s32(B + st * N * 128));
-      for (int s = 0; s < 4; s++)
-        mma(tmem + (it & 1) * N, ad + ((mode & 1) ? s * 2 : s * 16), bd + s * 16, idesc);
+      if (mode & 96) {  // interleave C independent accumulator chains (k-blocks to distinct D)
+        const int C = (mode & 32) ? 2 : 4;
+        for (int s = 0; s < 4; s++)
+          for (int j = 0; j < C; j++)
+            mma(tmem + j * N, desc_sw128(s32(A + ((it + j) & 3) * 16384)) + s * 2,
+                desc_none(s32(B + ((it + j) & 3) * N * 128)) + s * 16, idesc);
+        it += C - 1;
+      } else if (mode & 16) {
+        for (int s = 0; s < 4; s++)  // A from TMEM: columns 256 + 32*stage + 8*s
+          mma_ts(tmem + (it & 1) * N, tmem + 256 + st * 32 + s * 8, bd + s * 16, idesc);
+      } else {
+        for (int s = 0; s < 4; s++)
+          mma(tmem + (it & 1) * N, ad + ((mode & 1) ? s * 2 : s * 16), bd + s * 16, idesc);
+      }
       if (mode & 2) { commit(&bar); wait(&bar, ph); ph ^= 1; }
       if (mode & 8) commit(&bar2[it & 3]);  // commit only (async arrive), no wait
       if (mode & 4) {  // kernel-shaped sync per k-block (barriers pre-completed by a helper)
@@ -82,8 +98,12 @@ void run(long long* d) {
   const int smem = 4 * 16384 + 4 * N * 128;
   cudaFuncSetAttribute(probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* mn[] = {"A none ", "A sw128", "A none +commit/wait each", "A sw128+commit/wait each",
-                      "", "A sw128 + kernel-shaped sync", "", "", "", "A sw128 + commit only"};
-  for (int mode : {1, 3, 5, 9}) {
+                      "", "A sw128 + kernel-shaped sync", "", "", "", "A sw128 + commit only", "", "", "", "", "", "",
+                      "A TMEM", "", "", "", "A TMEM + kernel-shaped sync", "", "", "", "A TMEM + commit only", "", "", "", "", "", "", "", "", "2 chains", "", "", "", "", "", "", "", "", "", "", "", "", "", "", "",
+                      "", "", "", "", "", "", "", "", "", "", "", "", "", "", "", "", "4 chains", "", "", "", "4 chains + sync"};
+  for (int mode : {1, 5, 16, 33, 65, 65 + 4}) {
+    if (N > 128 && (mode & 16)) continue;
+    if (N > 128 && (mode & 64)) continue;
     const int iters = 2000;
     probe<N><<<1, 128, smem>>>(d, iters, mode);
     cudaError_t e = cudaDeviceSynchronize();

@@ -94,22 +94,26 @@ def main():
             t_fwd = timed(fwd, args.reps) / len(lays)
             t_gemm = timed(gemm, args.reps) / len(lays)
             row = {"model": args.model, "layer": s.name, "m": m, "n": s.n, "k": s.k,
-                   "q": s.act_bits, "kernel": "gemv_stream" if m <= 16 else "gemm_tc",
+                   "q": s.act_bits, "kernel": "gemv_stream" if m <= 32 else "gemm_tc",
                    "us_gemm": t_gemm * 1e3, "us_fwd": t_fwd * 1e3}
-            if m > 16 and not args.no_mma:
-                wsb = L.flexq_gemm_workspace_bytes(m, s.n, s.k, 128, -1)
+            def forced(ksplit, reps):  # the GEMM alone on a forced kernel route
+                wsb = L.flexq_gemm_workspace_bytes(m, s.n, s.k, 128, ksplit)
                 wss = [torch.zeros(wsb, dtype=torch.uint8, device=dev) for _ in lays]
 
-                def mma():
+                def run():
                     for lay, o, wsx in zip(lays, outs, wss):
                         frag, xs, corr, m_pad = lay._act_views(m)
                         _lib.check(L.flexq_gemm_t6(
                             _lib.ptr(lay.t6), _lib.ptr(lay.wscale), 1, frag, xs, corr, m, m_pad,
-                            s.n, s.k, 128, None, _lib.ptr(o), _lib.OUT_F16, _lib.ptr(wsx), -1,
+                            s.n, s.k, 128, None, _lib.ptr(o), _lib.OUT_F16, _lib.ptr(wsx), ksplit,
                             _lib.stream()))
 
-                row["us_mma_sync"] = timed(mma, max(3, args.reps // 4)) / len(lays) * 1e3
-                del wss
+                return timed(run, reps) / len(lays) * 1e3
+
+            if 16 < m <= 32:  # the tcgen05 kernel the streaming GEMV replaced here
+                row["us_tc"] = forced(-2, args.reps)
+            if m > 16 and not args.no_mma:
+                row["us_mma_sync"] = forced(-1, max(3, args.reps // 4))
             b = gemm_bytes(m, s.n, s.k)
             row["gbs_gemm"] = b / (t_gemm * 1e-3) / 1e9
             row["frac_hbm"] = row["gbs_gemm"] / peak

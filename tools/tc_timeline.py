@@ -15,7 +15,8 @@ def main():
     from paper_2508_04405_b200 import FlexQLinear, _lib
 
     m = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-    n, k = 13824, 5120
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 13824
+    k = int(sys.argv[3]) if len(sys.argv) > 3 else 5120
     w = torch.randn((n, k), device="cuda", dtype=torch.float16)
     lay = FlexQLinear(w, 6, 6, 128)
     x = torch.randn((m, k), device="cuda", dtype=torch.float16)
