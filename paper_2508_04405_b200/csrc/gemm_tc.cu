@@ -548,12 +548,14 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
           if constexpr (SF16) sw = __half2float(*reinterpret_cast<const __half*>(slot + sw_off));
           else sw = *reinterpret_cast<const float*>(slot + sw_off);
           const float2 sw2 = make_float2(sw, sw);
+          auto chunk = [&](auto cm2_tag) {  // (cmode branch hoisted out of the column loop)
+            constexpr bool CM2 = decltype(cm2_tag)::value;
 #pragma unroll
           for (int j = 0; j < CW; j += 4) {
             const int col = w0 + j;
             const float4 sv = *reinterpret_cast<const float4*>(sx + col);
             float4 cv;
-            if (cmode == 2) {
+            if constexpr (CM2) {
               const int4 c4 = *reinterpret_cast<const int4*>(cr + col);
               cv = make_float4(12582912.f + (float)(c4.x - kCorrBias), 12582912.f + (float)(c4.y - kCorrBias),
                                12582912.f + (float)(c4.z - kCorrBias), 12582912.f + (float)(c4.w - kCorrBias));
@@ -570,6 +572,9 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
             const float2 a23 = f2_fma(s23, f23, make_float2(acc[col + 2], acc[col + 3]));
             acc[col] = a01.x; acc[col + 1] = a01.y; acc[col + 2] = a23.x; acc[col + 3] = a23.y;
           }
+          };
+          if (cmode == 2) chunk(std::true_type{});
+          else chunk(std::false_type{});
         }
         if constexpr (TRACE) {
 #pragma unroll
@@ -722,6 +727,10 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
           if constexpr (SF16) sw = __half2float(*reinterpret_cast<const __half*>(slot + sw_off));
           else sw = *reinterpret_cast<const float*>(slot + sw_off);
           const float2 sw2 = make_float2(sw, sw);
+          // the column-constant mode is uniform per event: branch once, outside the loop, so the
+          // shared-memory table loads can be scheduled ahead of their uses
+          auto ev_loop = [&](auto cm2_tag) {
+            constexpr bool CM2 = decltype(cm2_tag)::value;
 #pragma unroll 1
           for (int c0 = 0; c0 < TN; c0 += 32) {
             // one TMEM round trip per 32 columns: partials (the MMA started the group from
@@ -741,7 +750,7 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
               for (int j = 0; j < 4; j++) {
                 const float4 sv = *reinterpret_cast<const float4*>(sx + cc + 4 * j);
                 float4 cv;
-                if (cmode == 2) {
+                if constexpr (CM2) {
                   const int4 c4 = *reinterpret_cast<const int4*>(cr + cc + 4 * j);
                   cv = make_float4(12582912.f + (float)(c4.x - kCorrBias), 12582912.f + (float)(c4.y - kCorrBias),
                                    12582912.f + (float)(c4.z - kCorrBias), 12582912.f + (float)(c4.w - kCorrBias));
@@ -774,6 +783,9 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
               }
             }
           }
+          };
+          if (cmode == 2) ev_loop(std::true_type{});
+          else ev_loop(std::false_type{});
         } else {  // trace only
 #pragma unroll 1
           for (int c0 = 0; c0 < TN; c0 += 16) {
