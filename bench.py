@@ -269,12 +269,20 @@ def main():
     except Exception:
         pass
     launches_per_fwd = 2  # fused activation quantizer + one GEMV/GEMM kernel per linear
+    # the automatic route (csrc/gemm_t6.cu): streaming GEMV for M <= 16, and for M <= 32 on
+    # layers of >= 8192 units (64 rows x 128 k); tcgen05 otherwise
+    streamed = [M <= 16 or (M <= 32 and -(-lay.n // 64) * -(-lay.k // 128) >= 8192) for _, lay in layers]
+    kern_gemv = "flexq::gemv_t6_stream_kernel"
+    kern_tc = "flexq::gemm_tc_kernel (tcgen05.mma kind::i8)"
+    kernel_label = kern_gemv if all(streamed) else kern_tc if not any(streamed) else \
+        f"{kern_gemv} + {kern_tc}"
+    dtype_label = ("int8 IMMA mma.sync" if all(streamed) else "int8 tcgen05.mma kind::i8"
+                   if not any(streamed) else "int8 IMMA mma.sync + tcgen05.mma kind::i8")
     line = {
         "metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": ("int8 IMMA mma.sync" if M <= 16 else "int8 tcgen05.mma kind::i8")
-                 + " (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue, fp16 out",
+        "dtype": dtype_label + " (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue, fp16 out",
         "data": "synthetic: random-init INT6 weights of the real shapes (fp16 N(0,1) quantized), fp16 N(0,1) activations",
         "config": {"workload": f"{args.model} decoder-layer linears qkv,o,gate,up (W6A6) + down (W6A8), M={M}",
                    "batch": M, "group_size": 128, "scales": "fp16",
@@ -286,8 +294,7 @@ def main():
         "hbm_GBps_algorithmic": layer_b / (ms_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("flexq::gemv_t6_stream_kernel" if M <= 16 else
-                                "flexq::gemm_tc_kernel (tcgen05.mma kind::i8)")
+                     "kernel": kernel_label
                                + f" ({len(shapes)} launches/step, per-launch bytes in DESIGN.md sec. 4)",
                      "peak_source": peak_kind, "gemm_us_per_step": ms_gemm * 1e3},
         "clocks": clk.summary(),

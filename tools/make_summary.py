@@ -27,7 +27,7 @@ def main(tag):
     out += ["## bench.py (LLaMA-2-70B decoder-layer linears, CUDA-graph step)", "",
             "| M | value (TOPS) | us/step | GEMM GB/s | roofline frac (of measured HBM) | e2e TOPS | CPU baseline TOPS (cores) | SM MHz |",
             "|---|---|---|---|---|---|---|---|"]
-    for m in ("m1", "m8", "m128"):
+    for m in ("m1", "m8", "m32", "m128"):
         p = os.path.join(src, f"{tag}_bench_{m}.json")
         if not os.path.exists(p):
             continue
@@ -53,12 +53,16 @@ def main(tag):
         shutil.copy(p, os.path.join(dst, f"{tag}_sweep_{mdl}.jsonl"))
         out += ["", f"## M sweep, {mdl} (tools/sweep.py; GEMM alone on quantized inputs, "
                     "weights rotated over > 2x L2)", "",
-                "| layer | N x K | M | kernel | GEMM us | fwd us | GB/s | frac HBM | TOPS | mma.sync us |",
-                "|---|---|---|---|---|---|---|---|---|---|"]
+                "| layer | N x K | M | kernel | GEMM us | fwd us | GB/s | frac HBM | TOPS | tcgen05 us (forced) | mma.sync us |",
+                "|---|---|---|---|---|---|---|---|---|---|---|"]
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from sweep import kernel_name
         for r in rows:
+            r["kernel"] = kernel_name(r["m"], r["n"], r["k"])
             out.append(f"| {r['layer']} | {r['n']}x{r['k']} | {r['m']} | {r['kernel']} | "
                        f"{r['us_gemm']:.1f} | {r['us_fwd']:.1f} | {r['gbs_gemm']:.0f} | "
                        f"{r['frac_hbm']:.2f} | {r['tops_gemm']:.1f} | "
+                       f"{r.get('us_tc', float('nan')):.1f} | "
                        f"{r.get('us_mma_sync', float('nan')):.1f} |")
     # decode
     p = os.path.join(src, f"{tag}_decode_7b.jsonl")

@@ -73,14 +73,14 @@ def summarize(tag: str, model: str):
     summary_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
     summary.setdefault("gemm_traffic_bytes_per_step", {})
-    for m in (1, 8, 64, 128, 256):
+    for m in (1, 8, 32, 64, 128, 256):
         rep = os.path.join(ROOT, "gpurun_out", f"{tag}_gemm_m{m}_raw.csv")
         if not os.path.exists(rep):
             rep = os.path.join(ROOT, "gpurun_out", f"{tag}_gemm_m{m}.ncu-rep")
         if not os.path.exists(rep):
             continue
         rows = raw_rows(rep)
-        kname = "gemv_t6_stream_kernel" if m <= 16 else "gemm_tc_kernel (tcgen05.mma kind::i8)"
+        kname = "gemv_t6_stream_kernel" if m <= 32 else "gemm_tc_kernel (tcgen05.mma kind::i8)"
         lines += [f"## M={m}: `ncu --set full` on the {len(rows)} {kname} launches of one step", "",
                   "| layer | " + " | ".join(lbl for _, lbl in KEYS) + " |",
                   "|---" * (len(KEYS) + 1) + "|"]

@@ -26,6 +26,12 @@ sys.path.insert(0, ROOT)
 L2_BYTES = 126 * 2**20
 
 
+def kernel_name(m, n, k):
+    """The automatic route of flexq_gemm_t6 at group 128 (csrc/gemm_t6.cu, gemv_stream.cu)."""
+    units = -(-n // 64) * -(-k // 128)
+    return "gemv_stream" if m <= 16 or (m <= 32 and units >= 8192) else "gemm_tc"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama2-13b")
@@ -94,7 +100,7 @@ def main():
             t_fwd = timed(fwd, args.reps) / len(lays)
             t_gemm = timed(gemm, args.reps) / len(lays)
             row = {"model": args.model, "layer": s.name, "m": m, "n": s.n, "k": s.k,
-                   "q": s.act_bits, "kernel": "gemv_stream" if m <= 32 else "gemm_tc",
+                   "q": s.act_bits, "kernel": kernel_name(m, s.n, s.k),
                    "us_gemm": t_gemm * 1e3, "us_fwd": t_fwd * 1e3}
             def forced(ksplit, reps):  # the GEMM alone on a forced kernel route
                 wsb = L.flexq_gemm_workspace_bytes(m, s.n, s.k, 128, ksplit)
