@@ -162,28 +162,44 @@ def main():
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
 
-    # column shards: rank r owns output rows [r*N/world, (r+1)*N/world) of every layer
-    layers, inputs, outs, gathered = [], {}, [], []
+    # Megatron pairing under torchrun (sharding.py): qkv/gate/up are
+    # column shards (rank r owns N/world output rows; replicated x; NCCL all-gather of the
+    # fp16 y shards), o/down are row shards (rank r owns K/world input columns on group
+    # boundaries; fp32 partial y; NCCL all-reduce).  world = 1: plain layers, no collective.
+    ROW_SHARDED = ("o_proj", "down_proj")
+    layers, inputs, outs, gathered, x_loc = [], {}, [], [], []
     for s in shapes:
-        n_loc = s.n // world
-        w = torch.randn((n_loc, s.k), generator=g, device=dev, dtype=torch.float16)
+        mode = "row" if (world > 1 and s.name in ROW_SHARDED) else "column"
+        n_loc, k_loc = (s.n, s.k // world) if mode == "row" else (s.n // world, s.k)
+        w = torch.randn((n_loc, k_loc), generator=g, device=dev, dtype=torch.float16)
         lay = FlexQLinear(w, 6, s.act_bits, 128, fp16_scales=True, layer_kind=policy_kind(s.name))
+        lay.mode = mode
         del w
         layers.append((s, lay))
         if s.k not in inputs:
             gx = torch.Generator(device=dev)
             gx.manual_seed(99 + s.k)  # same activations on every rank (replicated X)
             inputs[s.k] = torch.randn((M, s.k), generator=gx, device=dev, dtype=torch.float16)
-        outs.append(torch.empty((M, n_loc), dtype=torch.float16, device=dev))
+        x_loc.append(inputs[s.k][:, rank * k_loc:(rank + 1) * k_loc].contiguous()
+                     if mode == "row" else inputs[s.k])
+        outs.append(torch.empty((M, n_loc), device=dev,
+                                dtype=torch.float32 if mode == "row" else torch.float16))
         gathered.append(torch.empty((world, M, n_loc), dtype=torch.float16, device=dev)
-                        if world > 1 else None)
+                        if world > 1 and mode == "column" else None)
     torch.cuda.synchronize()
+
+    def collective(i, y):
+        if world == 1:
+            return
+        if layers[i][1].mode == "row":
+            dist.all_reduce(y, op=dist.ReduceOp.SUM)
+        else:
+            dist.all_gather_into_tensor(gathered[i], y)
 
     def step():
         for i, (s, lay) in enumerate(layers):
-            lay.forward(inputs[s.k], out=outs[i])
-            if world > 1:
-                dist.all_gather_into_tensor(gathered[i], outs[i])
+            lay.forward(x_loc[i], out=outs[i])
+            collective(i, outs[i])
 
     def gemm_step():
         for i, (s, lay) in enumerate(layers):
@@ -267,9 +283,16 @@ def main():
         for k_, hv in host_in.items():
             dev_in[k_].copy_(hv, non_blocking=True)
         for i, (s, lay) in enumerate(layers):
-            y = lay(dev_in[s.k])
-            dist.all_gather_into_tensor(gathered[i], y)
-            y = gathered[i].permute(1, 0, 2).reshape(M, -1)
+            if lay.mode == "row":
+                kl = s.k // world
+                y = lay(dev_in[s.k][:, rank * kl:(rank + 1) * kl].contiguous(),
+                        out_dtype=torch.float32)
+                dist.all_reduce(y, op=dist.ReduceOp.SUM)
+                y = y.half()
+            else:
+                y = lay(dev_in[s.k])
+                dist.all_gather_into_tensor(gathered[i], y)
+                y = gathered[i].permute(1, 0, 2).reshape(M, -1)
             host_out[i].copy_(y, non_blocking=True)
 
     for _ in range(5):
@@ -278,7 +301,7 @@ def main():
 
     flops_total = sum(2 * M * s.n * s.k for s in shapes)  # whole job (all ranks)
     tops = flops_total / (ms_step * 1e-3) / 1e12
-    gbytes_loc = sum(gemm_bytes(M, lay.n, s.k) for s, lay in layers)
+    gbytes_loc = sum(gemm_bytes(M, lay.n, lay.k) for s, lay in layers)
     layer_b = sum(layer_bytes(M, s.n, s.k) for s in shapes)
     peak, peak_kind = hbm_peak()
     achieved = gbytes_loc / (ms_gemm * 1e-3) / 1e9
@@ -309,7 +332,9 @@ def main():
         "data": "synthetic: random-init INT6 weights of the real shapes (fp16 N(0,1) quantized), fp16 N(0,1) activations",
         "config": {"workload": f"{args.model} decoder-layer linears qkv,o,gate,up (W6A6) + down (W6A8), M={M}",
                    "batch": M, "group_size": 128, "scales": "fp16",
-                   "parallelism": f"column-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                   "parallelism": (f"tp{world}: qkv/gate/up column shards + NCCL all-gather, "
+                                   f"o/down row shards (fp32 partials) + NCCL all-reduce")
+                                  if world > 1 else "single GPU",
                    "l2": "weights 642 MB/step > 126 MB L2 (no flush needed)",
                    "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks"},
         "latency_us_per_step": ms_step * 1e3,

@@ -37,6 +37,7 @@ extern "C" {
 /* device flag bits written by the quantizers */
 #define FLEXQ_FLAG_NONFINITE 1u      /* quantize.py:135-136 "input contains non-finite values" */
 #define FLEXQ_FLAG_NONPOS_SCALE 2u   /* quantize.py:71-72   "all scales must be strictly positive" */
+#define FLEXQ_FLAG_KV_OVERFLOW 4u    /* decode harness: a position at or past the KV-cache length */
 
 /* float input dtypes */
 #define FLEXQ_DT_F16 0
@@ -171,11 +172,15 @@ int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, 
                          const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
                          uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
                          cudaStream_t stream);
-/* Same with a fused fp16 residual [m, n] (may alias y): y = x W^T + residual. */
+/* Same with the output dtype chosen (FLEXQ_OUT_F16 / FLEXQ_OUT_F32 y [m, n]) and an optional
+ * fused residual of that dtype [m, n] (may alias y): y = x W^T + residual.  FLEXQ_OUT_F32 is
+ * what a row (K) shard emits: its fp32 partial y is summed across ranks before any rounding
+ * (the reference's group partials combine in the float epilogue,
+ * engine.py:277-286). */
 int flexq_linear_forward_ex(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
                             const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
-                            uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
-                            const void* residual, cudaStream_t stream);
+                            void* y, int out_dtype, void* act_buf, void* workspace,
+                            uint32_t* flag, const void* residual, cudaStream_t stream);
 
 /* ---- LLaMA-2 decode harness (BASELINE config 5) ---------
  * Producers and glue around the W6Ax linears for an end-to-end decode step.  The
@@ -195,19 +200,22 @@ int flexq_silu_mul_quantize(const void* gate_up, int64_t x_stride, int64_t rows,
                             cudaStream_t stream);
 /* Rotate-half RoPE of q and k for each token's position pos[b] (device int32), k and v
  * appended to the caches [batch, heads, max_len, head_dim] at pos[b]; q_out [batch, heads,
- * head_dim].  qkv rows are [q | k | v] (heads * head_dim each). */
+ * head_dim].  qkv rows are [q | k | v] (heads * head_dim each).  A position outside
+ * [0, max_len) writes nothing (attention then reads at most max_len cached positions). */
 int flexq_rope_kv_append(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache,
                          void* q_out, int64_t batch, int heads, int head_dim, int64_t max_len,
                          float theta, cudaStream_t stream);
 /* The whole attention block of a decode step in one kernel: RoPE + append (as above),
- * attention, and the o_proj activation quantizer (head_dim 128 = group size, so head h of
- * token b is group h): writes o_proj's operand (act_frag / act_scale / act_corr with
- * m_pad = flexq_act_m_pad(batch)), bit-identical to flexq_quantize of the fp16 attention
- * output, which is also stored to out[batch, heads * head_dim] when out is not NULL. */
+ * attention, and the o_proj activation quantizer (group_size must equal head_dim = 128, so
+ * head h of token b is group h; anything else is FLEXQ_ERR_CONFIG): writes o_proj's operand
+ * (act_frag / act_scale / act_corr with m_pad = flexq_act_m_pad(batch)), bit-identical to
+ * flexq_quantize of the fp16 attention output, which is also stored to
+ * out[batch, heads * head_dim] when out is not NULL.  A position outside [0, max_len) sets
+ * FLEXQ_FLAG_KV_OVERFLOW in *flag and writes nothing for that token. */
 int flexq_attn_block(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache, void* out,
                      int64_t batch, int heads, int head_dim, int64_t max_len, float theta,
-                     int bits, uint32_t* act_frag, float* act_scale, int32_t* act_corr,
-                     int64_t m_pad, uint32_t* flag, cudaStream_t stream);
+                     int bits, int64_t group_size, uint32_t* act_frag, float* act_scale,
+                     int32_t* act_corr, int64_t m_pad, uint32_t* flag, cudaStream_t stream);
 /* Single-query attention of q over cache positions [0, pos[b]] (head_dim 128). */
 int flexq_attn_decode(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
                       void* out, int64_t batch, int heads, int head_dim, int64_t max_len,

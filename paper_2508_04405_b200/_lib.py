@@ -15,7 +15,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FLEXQ_LIB") or os.path.join(_PKG, "_lib", "libflexq_sm100a.so")
 
 OK, ERR_INVALID, ERR_SHAPE, ERR_CONFIG, ERR_FORMAT, ERR_CUDA = 0, -1, -2, -3, -4, -5
-FLAG_NONFINITE, FLAG_NONPOS_SCALE = 1, 2
+FLAG_NONFINITE, FLAG_NONPOS_SCALE, FLAG_KV_OVERFLOW = 1, 2, 4
 DT_F16, DT_BF16, DT_F32, DT_F64 = 0, 1, 2, 3
 OUT_F16, OUT_F32 = 0, 1
 
@@ -47,15 +47,15 @@ SIGNATURES = {
     "flexq_popcount_and": (i32, [vp, vp, i64, vp, vp]),
     "flexq_act_buf_bytes": (i64, [i64, i64, i64]),
     "flexq_linear_forward": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, vp, vp, vp, vp]),
-    "flexq_linear_forward_ex": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, vp, vp, vp, vp,
-                                      vp]),
+    "flexq_linear_forward_ex": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, i32, vp, vp, vp,
+                                      vp, vp]),
     "flexq_rmsnorm_quantize": (i32, [vp, i64, vp, ctypes.c_float, i64, i64, i32, i64, vp, vp, vp,
                                      i64, vp, vp, vp]),
     "flexq_silu_mul_quantize": (i32, [vp, i64, i64, i64, i32, i64, vp, vp, vp, i64, vp, vp, vp]),
     "flexq_rope_kv_append": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, ctypes.c_float, vp]),
     "flexq_attn_decode": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, vp]),
-    "flexq_attn_block": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, ctypes.c_float, i32, vp, vp,
-                               vp, i64, vp, vp]),
+    "flexq_attn_block": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, ctypes.c_float, i32, i64,
+                               vp, vp, vp, i64, vp, vp]),
 }
 
 _lib = None

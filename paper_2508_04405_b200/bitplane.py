@@ -101,11 +101,12 @@ def bit_planes(values, bits: int, signed: bool = True) -> BitPlaneSet:
     if values.ndim == 1:
         values = values[None, :]
     t = _dev.torch()
-    codes = _dev.to_device(values, t.int16)
     lo, hi = ((-(1 << (bits - 1)), (1 << (bits - 1)) - 1) if signed else (0, (1 << bits) - 1))
-    if codes.numel() and (int(codes.min()) < lo or int(codes.max()) > hi):
+    # range-check in the input's own integer type, before narrowing (65539 must not wrap to 3)
+    if (values.numel() if is_t else values.size) and (int(values.min()) < lo or int(values.max()) > hi):
         raise InvalidInputError(
             f"values outside the {'signed' if signed else 'unsigned'} {bits}-bit range [{lo}, {hi}]")
+    codes = _dev.to_device(values, t.int16)
     return BitPlaneSet(None, plane_coeffs(bits, signed), bits, signed, _codes=codes,
                        _numpy=not is_t)
 

@@ -48,7 +48,8 @@ int rope_kv_append_launch(const void*, const int*, void*, void*, void*, int64_t,
 int attn_decode_launch(const void*, const void*, const void*, const int*, void*, int64_t, int, int,
                        int64_t, cudaStream_t);
 int attn_block_launch(const void*, const int*, void*, void*, void*, int64_t, int, int, int64_t,
-                      float, int, uint32_t*, float*, int32_t*, int64_t, uint32_t*, cudaStream_t);
+                      float, int, int64_t, uint32_t*, float*, int32_t*, int64_t, uint32_t*,
+                      cudaStream_t);
 int group_epilogue_launch(const int32_t*, const double*, const double*, int64_t, int64_t, int64_t,
                           double*, uint16_t*, cudaStream_t);
 
@@ -243,10 +244,14 @@ int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size) {
 
 static int linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
                           const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
-                          uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
+                          void* y, int out_dtype, void* act_buf, void* workspace, uint32_t* flag,
                           const void* residual, cudaStream_t stream) {
   if (!act_buf || !flag || !y) {
     set_error("linear_forward: act_buf, flag and y are required");
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  if (out_dtype != FLEXQ_OUT_F16 && out_dtype != FLEXQ_OUT_F32) {
+    set_error("linear_forward: unknown out_dtype %d", out_dtype);
     return FLEXQ_ERR_INVALID_INPUT;
   }
   const int64_t m_pad = flexq_act_m_pad(m);
@@ -261,23 +266,23 @@ static int linear_forward(const uint32_t* t6, const void* wscale, int scale_f16,
                            act_frag, xs, corr, m_pad, flag, stream);
   if (rc) return rc;
   return gemm_t6_launch(t6, wscale, scale_f16, act_frag, xs, corr, m, m_pad, n, k, group_size,
-                        nullptr, y, FLEXQ_OUT_F16, workspace, 0, residual, stream);
+                        nullptr, y, out_dtype, workspace, 0, residual, stream);
 }
 
 int flexq_linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
                          const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
                          uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
                          cudaStream_t stream) {
-  return linear_forward(t6, wscale, scale_f16, xbits, x, m, n, k, group_size, y, act_buf,
-                        workspace, flag, nullptr, stream);
+  return linear_forward(t6, wscale, scale_f16, xbits, x, m, n, k, group_size, y, FLEXQ_OUT_F16,
+                        act_buf, workspace, flag, nullptr, stream);
 }
 
 int flexq_linear_forward_ex(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
                             const void* x, int64_t m, int64_t n, int64_t k, int64_t group_size,
-                            uint16_t* y, void* act_buf, void* workspace, uint32_t* flag,
-                            const void* residual, cudaStream_t stream) {
-  return linear_forward(t6, wscale, scale_f16, xbits, x, m, n, k, group_size, y, act_buf,
-                        workspace, flag, residual, stream);
+                            void* y, int out_dtype, void* act_buf, void* workspace,
+                            uint32_t* flag, const void* residual, cudaStream_t stream) {
+  return linear_forward(t6, wscale, scale_f16, xbits, x, m, n, k, group_size, y, out_dtype,
+                        act_buf, workspace, flag, residual, stream);
 }
 
 /* ---- LLaMA decode harness (BASELINE config 5) ---- */
@@ -312,10 +317,10 @@ int flexq_attn_decode(const void* q, const void* k_cache, const void* v_cache, c
 
 int flexq_attn_block(const void* qkv, const int32_t* pos, void* k_cache, void* v_cache, void* out,
                      int64_t batch, int heads, int head_dim, int64_t max_len, float theta,
-                     int bits, uint32_t* act_frag, float* act_scale, int32_t* act_corr,
-                     int64_t m_pad, uint32_t* flag, cudaStream_t stream) {
+                     int bits, int64_t group_size, uint32_t* act_frag, float* act_scale,
+                     int32_t* act_corr, int64_t m_pad, uint32_t* flag, cudaStream_t stream) {
   return attn_block_launch(qkv, pos, k_cache, v_cache, out, batch, heads, head_dim, max_len, theta,
-                           bits, act_frag, act_scale, act_corr, m_pad, flag, stream);
+                           bits, group_size, act_frag, act_scale, act_corr, m_pad, flag, stream);
 }
 
 }  // extern "C"

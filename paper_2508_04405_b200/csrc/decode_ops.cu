@@ -21,6 +21,7 @@ __global__ void rope_kv_append_kernel(const __half* __restrict__ qkv, const int*
   const int b = blockIdx.y, hh = blockIdx.x, i = threadIdx.x;  // i < D/2
   const int half = D / 2;
   const int p = pos[b];
+  if (p < 0 || p >= Lmax) return;  // no slot: the cache is full (the host raises first)
   const float inv_freq = powf(theta, -2.f * (float)i / (float)D);
   float sn, cs;
   sincosf((float)p * inv_freq, &sn, &cs);
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_decode_kernel(
   pdl_wait();
   const int b = blockIdx.y, hh = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int len = pos[b] + 1;
+  const int len = min(pos[b] + 1, Lmax);  // never read past the cache
   const __half* qp = q + ((int64_t)b * H + hh) * D + lane * 4;
   const uint2 qraw = *reinterpret_cast<const uint2*>(qp);
   const float2 qa = __half22float2(*reinterpret_cast<const __half2*>(&qraw.x));
@@ -124,6 +125,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_block_kernel(
   const int b = blockIdx.y, hh = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int p = pos[b];
+  if (p < 0 || p >= Lmax) {  // KV cache full: flag it, touch nothing
+    if (tid == 0) atomicOr(flag, FLEXQ_FLAG_KV_OVERFLOW);
+    return;
+  }
   const int64_t head_base = ((int64_t)b * H + hh) * Lmax * D;
   if (tid < D / 2) {  // RoPE (rotate-half) + append
     const int i = tid;
@@ -230,8 +235,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_block_kernel(
 
 int attn_block_launch(const void* qkv, const int* pos, void* k_cache, void* v_cache, void* out,
                       int64_t batch, int heads, int head_dim, int64_t lmax, float theta, int bits,
-                      uint32_t* act_frag, float* act_scale, int32_t* act_corr, int64_t m_pad,
-                      uint32_t* flag, cudaStream_t st) {
+                      int64_t group_size, uint32_t* act_frag, float* act_scale, int32_t* act_corr,
+                      int64_t m_pad, uint32_t* flag, cudaStream_t st) {
+  if (group_size != head_dim) {
+    set_error("attn_block: the fused o_proj quantizer needs group_size == head_dim (%d), got %lld",
+              head_dim, (long long)group_size);
+    return FLEXQ_ERR_CONFIG;
+  }
   if (head_dim != 128 || batch < 1 || heads < 1 || lmax < 1 || bits < 2 || bits > 8 ||
       !act_frag || !act_scale || !act_corr || !flag || m_pad < batch || m_pad % 8) {
     set_error("attn_block: needs head_dim 128 (= the quantizer group) and an operand buffer");

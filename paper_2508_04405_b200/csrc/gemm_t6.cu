@@ -285,8 +285,12 @@ static void dispatch_t6(const T6Params& p, bool sf16, bool trace, bool fast, int
 
 constexpr int64_t kT6TokChunk = 64;  // 8 mma n-tiles per launch
 
-static int64_t ws_counters_offset(int64_t ksplit, int64_t m_pad, int64_t rt) {
-  const int64_t mc = m_pad < kT6TokChunk ? m_pad : kT6TokChunk;
+// Counters sit after the fp32 split partials of one token chunk.  Sized and located from the
+// token count m alone (never from a caller's m_pad, which may be a whole tcgen05 tile), so
+// gemm_t6_workspace and gemm_t6_launch agree for every caller.
+static int64_t ws_counters_offset(int64_t ksplit, int64_t m, int64_t rt) {
+  const int64_t m8 = cdiv(m, kTokTile) * kTokTile;
+  const int64_t mc = m8 < kT6TokChunk ? m8 : kT6TokChunk;
   return cdiv(ksplit * mc * rt * kRowTile * 4, 256) * 256;
 }
 
@@ -321,9 +325,7 @@ static bool tc_enabled() {
 int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int ksplit) {
   T6Geom G(n, k, gs);
   const int ks_eff = ksplit <= 0 ? auto_ksplit_t6(G.rt, G.kb) : ksplit;
-  const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
-  const int64_t mc = m_pad < kT6TokChunk ? m_pad : kT6TokChunk;
-  int64_t bytes = ws_counters_offset(ks_eff, mc, G.rt) + cdiv(G.rt * 4, 256) * 256;
+  int64_t bytes = ws_counters_offset(ks_eff, m, G.rt) + cdiv(G.rt * 4, 256) * 256;
   if ((ksplit == -3 && gemv_stream_supported(m, G.spg, INT64_MAX)) ||
       (ksplit <= 0 && (ksplit == 0 || m <= 16) && gemv_stream_supported(m, G.spg, G.rg * G.kb))) {
     const int64_t b2 = gemv_stream_workspace(m, n, k, gs);
@@ -423,7 +425,7 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
     p.y = y;
     p.ws_part = reinterpret_cast<float*>(workspace);
     p.counters = workspace ? reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) +
-                                                         ws_counters_offset(ksplit, m_pad, G.rt))
+                                                         ws_counters_offset(ksplit, m, G.rt))
                            : nullptr;
     p.ksplit = ksplit;
     p.res = residual;

@@ -123,16 +123,29 @@ class FlexQLinear:
         return cls(obj, group_size=group_size, **kw)
 
     # -- buffers ------------------------------------------------------------------------
-    def buffers(self, m: int):
-        if m not in self._bufs:
-            t = _dev.torch()
+    def buffers(self, m: int, stream: int | None = None):
+        """(act buffer, workspace) for batch m on ``stream`` (default: the current stream).
+
+        Each stream gets its own pair: the quantizer writes the act buffer and the GEMM's
+        split fixups count in the workspace, so two forwards in flight on different streams
+        must not share them.  The workspace counters are zeroed once here and every launch
+        leaves them zeroed (graph-safe).  A CUDA-graph capture (its own side stream) reuses the
+        buffers of a stream that already ran this batch eagerly, so the graph's replays and
+        eager forwards on that stream must be stream-ordered."""
+        t = _dev.torch()
+        key = (m, _lib.stream() if stream is None else stream)
+        if key not in self._bufs:
+            if t.cuda.is_current_stream_capturing():
+                for (mm, _), bufs in self._bufs.items():
+                    if mm == m:
+                        return bufs
             L = _lib.lib()
             act = t.empty(L.flexq_act_buf_bytes(m, self.k, self.group_size), dtype=t.uint8,
                           device=self.device)
             ws = t.zeros(max(L.flexq_gemm_workspace_bytes(m, self.n, self.k, self.group_size, 0), 16),
                          dtype=t.uint8, device=self.device)
-            self._bufs[m] = (act, ws)
-        return self._bufs[m]
+            self._bufs[key] = (act, ws)
+        return self._bufs[key]
 
     @property
     def weight_bytes(self) -> int:
@@ -140,22 +153,49 @@ class FlexQLinear:
         return self.t6.numel() * 4 + self.wscale.numel() * self.wscale.element_size()
 
     # -- forward --------------------------------------------------------------------------
-    def forward(self, x, out=None, residual=None):
-        """x: fp16 CUDA [M, K] -> fp16 CUDA [M, N] (no host sync).  ``residual`` (fp16
-        [M, N], may be ``out`` itself) is added in the GEMM epilogue."""
+    def _check_out(self, what: str, buf, m: int, dtype) -> None:
+        if not (_dev.is_torch(buf) and buf.is_cuda and buf.device == self.device):
+            raise InvalidInputError(f"{what} must be a CUDA tensor on {self.device}")
+        if buf.dtype != dtype:
+            raise InvalidInputError(f"{what} must be {dtype}, got {buf.dtype}")
+        if tuple(buf.shape) != (m, self.n) or not buf.is_contiguous():
+            raise ShapeError(f"{what} must be a contiguous [{m}, {self.n}] tensor, got "
+                             f"{tuple(buf.shape)}{'' if buf.is_contiguous() else ' (strided)'}")
+
+    def forward(self, x, out=None, residual=None, out_dtype=None):
+        """x: fp16 CUDA [M, K] -> [M, N] on the layer's device (no host sync).
+
+        ``out_dtype`` is torch.float16 (default) or torch.float32 (an unrounded fp32 y: the
+        partial a row shard sums across ranks).  ``residual`` ([M, N] of the output dtype,
+        may be ``out`` itself) is added in the GEMM epilogue."""
         t = _dev.torch()
+        if not _dev.is_torch(x):
+            raise InvalidInputError("x must be a torch tensor (use quantized_linear for arrays)")
         if x.dim() != 2 or x.shape[1] != self.k:
             raise ShapeError(f"activation shape {tuple(x.shape)} does not match K={self.k}")
+        if not x.is_cuda or x.device != self.device:
+            raise InvalidInputError(f"x must be a CUDA tensor on {self.device}, got {x.device}")
+        if out_dtype is None:
+            out_dtype = out.dtype if out is not None else t.float16
+        if out_dtype not in (t.float16, t.float32):
+            raise InvalidInputError(f"out_dtype must be float16 or float32, got {out_dtype}")
         if x.dtype != t.float16:
             x = x.to(t.float16)
         x = x.contiguous()
         m = x.shape[0]
+        if m < 1:
+            raise ShapeError("activation batch must be at least one row")
         if out is None:
-            out = t.empty((m, self.n), dtype=t.float16, device=self.device)
+            out = t.empty((m, self.n), dtype=out_dtype, device=self.device)
+        else:
+            self._check_out("out", out, m, out_dtype)
+        if residual is not None:
+            self._check_out("residual", residual, m, out_dtype)
         act, ws = self.buffers(m)
         _lib.check(_lib.lib().flexq_linear_forward_ex(
             _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), self.activation_bits,
-            _lib.ptr(x), m, self.n, self.k, self.group_size, _lib.ptr(out), _lib.ptr(act),
+            _lib.ptr(x), m, self.n, self.k, self.group_size, _lib.ptr(out),
+            _lib.OUT_F32 if out_dtype == t.float32 else _lib.OUT_F16, _lib.ptr(act),
             _lib.ptr(ws), _lib.ptr(self.flag), _lib.ptr(residual), _lib.stream()))
         return out
 
@@ -176,11 +216,16 @@ class FlexQLinear:
         """Re-run only the T6 GEMM on the activations quantized by the last forward(m).
 
         Used by bench.py to time the dominant kernel alone (roofline)."""
+        t = _dev.torch()
+        self._check_out("out", out, m, out.dtype if out.dtype in (t.float16, t.float32) else t.float16)
+        if residual is not None:
+            self._check_out("residual", residual, m, out.dtype)
         frag, xs, corr, m_pad = self._act_views(m)
         _, ws = self.buffers(m)
         _lib.check(_lib.lib().flexq_gemm_t6_ex(
             _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), frag, xs, corr, m,
-            m_pad, self.n, self.k, self.group_size, None, _lib.ptr(out), _lib.OUT_F16,
+            m_pad, self.n, self.k, self.group_size, None, _lib.ptr(out),
+            _lib.OUT_F32 if out.dtype == t.float32 else _lib.OUT_F16,
             _lib.ptr(ws), 0, _lib.ptr(residual), _lib.stream()))
         return out
 

@@ -20,6 +20,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import _dev, _lib
+from .errors import ConfigError, InvalidInputError
 from .linear import FlexQLinear
 from .quantize import DEFAULT_POLICY, BitPolicy, activation_bits
 
@@ -80,7 +81,12 @@ class FlexQLlamaDecoder:
         gen = t.Generator(device=dev)
         gen.manual_seed(seed)
         h, f, H, D = cfg.hidden, cfg.ffn, cfg.heads, cfg.head_dim
-        assert H * D == h, "hidden must equal heads * head_dim"
+        if H * D != h:
+            raise ConfigError(f"hidden ({h}) must equal heads * head_dim ({H} * {D})")
+        if group_size != D:
+            # flexq_attn_block quantizes o_proj's input with head h of a token as group h
+            raise ConfigError(f"the decode step fuses o_proj's quantizer into attention and needs "
+                              f"group_size == head_dim ({D}), got {group_size}")
         if weights_from is not None:  # share the quantized weights (another batch size)
             src = weights_from
             self.embed, self.layers, self.norm_f, self.lm_head = (src.embed, src.layers, src.norm_f,
@@ -108,6 +114,7 @@ class FlexQLlamaDecoder:
             for lin in (lay.qkv, lay.o, lay.gate_up, lay.down):
                 lin.buffers(B)
         self._graph = None
+        self.steps_taken = 0  # host mirror of the device positions (all start at 0 on reset)
 
     @property
     def weight_bytes(self) -> int:
@@ -148,8 +155,8 @@ class FlexQLlamaDecoder:
             _lib.check(L.flexq_attn_block(
                 _lib.ptr(self.qkv_out), _lib.ptr(self.pos), _lib.ptr(self.k_cache[li]),
                 _lib.ptr(self.v_cache[li]), _lib.ptr(self.attn) if rec is not None else None, B,
-                cfg.heads, cfg.head_dim, self.max_len, cfg.rope_theta, lay.o.activation_bits, frag,
-                xs, corr, m_pad, _lib.ptr(self.flag), _lib.stream()))
+                cfg.heads, cfg.head_dim, self.max_len, cfg.rope_theta, lay.o.activation_bits,
+                self.group_size, frag, xs, corr, m_pad, _lib.ptr(self.flag), _lib.stream()))
             lay.o.gemm_only(B, self.x, residual=self.x)  # x += o(attn), residual fused
             h2 = t.empty_like(self.x) if rec is not None else None
             self._fused_quant("rmsnorm", self.x, lay.gate_up, cfg.hidden, lay.norm2, h2)
@@ -200,6 +207,7 @@ class FlexQLlamaDecoder:
     def reset(self, tokens=None):
         t = _dev.torch()
         self.pos.zero_()
+        self.steps_taken = 0
         if tokens is None:
             self.tokens.copy_(t.arange(self.batch, device=self.device) % self.cfg.vocab)
         else:
@@ -225,6 +233,10 @@ class FlexQLlamaDecoder:
 
     def step(self):
         """Decode one token per sequence (graph replay when captured)."""
+        if self.steps_taken >= self.max_len:
+            raise InvalidInputError(f"KV cache full: {self.max_len} positions decoded "
+                                    f"(max_len={self.max_len}); reset() or use a longer cache")
+        self.steps_taken += 1
         if self._graph is not None:
             self._graph.replay()
         else:
@@ -232,9 +244,9 @@ class FlexQLlamaDecoder:
         return self.tokens
 
     def check_errors(self) -> None:
-        from .errors import InvalidInputError
-
         bits = int(self.flag.item())
         self.flag.zero_()
+        if bits & _lib.FLAG_KV_OVERFLOW:
+            raise InvalidInputError("KV cache overflow: a position reached max_len")
         if bits:
             raise InvalidInputError("non-finite activations in the decode step")

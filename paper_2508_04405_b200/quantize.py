@@ -63,10 +63,11 @@ class QuantTensor:
         lim = qmax(self.bits)
         if _dev.is_torch(self.values):
             ok_scales = bool((self.scales > 0).all()) if self.scales.numel() else True
-            ok_vals = bool((self.values.abs() <= lim).all()) if self.values.numel() else True
+            ok_vals = (bool((self.values.to(_dev.torch().int64).abs() <= lim).all())
+                       if self.values.numel() else True)  # widen first: abs(int8 -128) wraps
         else:
             ok_scales = bool(np.all(np.asarray(self.scales) > 0))
-            ok_vals = not np.any(np.abs(np.asarray(self.values).astype(np.int16)) > lim)
+            ok_vals = not np.any(np.abs(np.asarray(self.values).astype(np.int64)) > lim)
         if not ok_scales:
             raise InvalidInputError("all scales must be strictly positive")
         if not ok_vals:

@@ -6,19 +6,21 @@ north-star plan:
 
 * column (N) sharding -- rank r owns output rows [r*N/P, (r+1)*N/P).  X is
   replicated, every rank quantizes it identically, computes its y shard, and
-  one all-gather assembles y.  The result is bit-identical for every P because
-  each output element is computed by exactly one rank with the same kernel.
-  Used for qkv/o/gate/up.
+  one all-gather assembles y.  Every output element is computed by exactly one
+  rank, so the gather is exact.  Used for qkv/gate/up.
 * row (K) sharding -- rank r owns the K range [r*K/P, (r+1)*K/P), which must
   fall on scale-group boundaries so INT32 group partials stay exact.  Each
   rank quantizes its slice of x (groups are local), computes an fp32 partial
   y over its K range, and an all-reduce (sum) combines them.  Partials per
   group are exact; only the float sum order differs from P = 1 (within the
-  fp16 tolerance).  Used for down_proj (Megatron pairing).
+  fp16 tolerance).  Used for o_proj and down_proj, which consume the column-
+  sharded outputs of qkv/attention and gate/up (the Megatron pairing).
 
 The collective sits only at the shard boundary.  ``local`` is the per-rank
-compute (FlexQLinear on the GPU); tests inject the CPU oracle to exercise the
-partitioning and collectives with gloo on CPU.
+compute (FlexQLinear on the GPU; row shards ask it for an unrounded fp32 y, so
+nothing is rounded to fp16 before the sum); tests also inject the CPU oracle to
+exercise the partitioning and collectives with gloo on CPU.  Over gloo, CUDA
+results are staged through host memory for the collective (NCCL needs none).
 """
 from __future__ import annotations
 
@@ -91,9 +93,12 @@ class ShardedLinear:
             w = shard_weight(weight, spec)
             lin = FlexQLinear(w.contiguous() if hasattr(w, "contiguous") else w, 6,
                               activation_bits, spec.group_size, fp16_scales=fp16_scales)
-            out_dtype = "f32" if spec.mode == "row" else "f16"
-            local = (lambda x, _lin=lin: _lin(x)) if out_dtype == "f16" else \
-                (lambda x, _lin=lin: _lin(x).float())
+            import torch
+
+            # row shards: fp32 partial y straight from the GEMM epilogue (no fp16 rounding
+            # before the cross-rank sum); column shards: the final fp16 y
+            out_dtype = torch.float32 if spec.mode == "row" else torch.float16
+            local = (lambda x, _lin=lin, _dt=out_dtype: _lin(x, out_dtype=_dt))
         self.local = local
 
     def __call__(self, x):
@@ -105,11 +110,16 @@ class ShardedLinear:
         y = self.local(x_loc)
         if s.world == 1:
             return y
+        dev = y.device
+        stage = y.is_cuda and dist.get_backend(self.group) == "gloo"
+        if stage:
+            y = y.cpu()
         if s.mode == "column":
             m, n_loc = y.shape
             buf = torch.empty((s.world * m, n_loc), dtype=y.dtype, device=y.device)
             dist.all_gather_into_tensor(buf, y.contiguous(), group=self.group)
-            return buf.view(s.world, m, n_loc).permute(1, 0, 2).reshape(m, s.world * n_loc)
-        y = y.contiguous()
-        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
-        return y
+            y = buf.view(s.world, m, n_loc).permute(1, 0, 2).reshape(m, s.world * n_loc)
+        else:
+            y = y.contiguous()
+            dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
+        return y.to(dev) if stage else y

@@ -208,7 +208,7 @@ def test_attn_block_matches_separate_ops():
                                        _lib.ptr(pos), _lib.ptr(out_a), B, H, D, Lmax, _lib.stream()))
         _lib.check(L.flexq_attn_block(_lib.ptr(qkv), _lib.ptr(pos), _lib.ptr(caches[2]),
                                       _lib.ptr(caches[3]), _lib.ptr(out_b), B, H, D, Lmax, 10000.0, 6,
-                                      _lib.ptr(frag), _lib.ptr(xs), _lib.ptr(corr), m_pad,
+                                      128, _lib.ptr(frag), _lib.ptr(xs), _lib.ptr(corr), m_pad,
                                       _lib.ptr(flag), _lib.stream()))
     torch.cuda.synchronize()
     assert torch.equal(caches[0], caches[2]) and torch.equal(caches[1], caches[3])
@@ -216,3 +216,38 @@ def test_attn_block_matches_separate_ops():
     frag2, xs2, corr2, _ = _act_from_quantize(out_b, 6, None)
     assert torch.equal(frag, frag2) and torch.equal(xs[:, :B], xs2[:, :B])
     assert torch.equal(corr[:, :B], corr2[:, :B])
+
+
+def test_attn_block_rejects_group_and_guards_kv_bound():
+    """Advisor findings: a group size other than head_dim is a ConfigError, and a position at
+    max_len sets FLEXQ_FLAG_KV_OVERFLOW instead of writing past the cache."""
+    L = _lib.lib()
+    B, H, D, Lmax = 2, 2, 128, 4
+    n = B * H * Lmax * D
+    kbuf = torch.zeros(n + 4096, dtype=torch.float16, device="cuda")  # cache + guard region
+    vbuf = torch.zeros_like(kbuf)
+    kc, vc = kbuf[:n].view(B, H, Lmax, D), vbuf[:n].view(B, H, Lmax, D)
+    m_pad = L.flexq_act_m_pad(B)
+    frag = torch.zeros(L.flexq_act_frag_bytes(m_pad, H * D, 128) // 4, dtype=torch.int32, device="cuda")
+    xs = torch.zeros((H, m_pad), dtype=torch.float32, device="cuda")
+    corr = torch.zeros((H, m_pad), dtype=torch.int32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    qkv = torch.randn((B, 3 * H * D), device="cuda").half()
+    pos = torch.tensor([Lmax, 1], dtype=torch.int32, device="cuda")
+    args = (_lib.ptr(qkv), _lib.ptr(pos), _lib.ptr(kc), _lib.ptr(vc), None, B, H, D, Lmax, 10000.0, 6)
+    tail = (_lib.ptr(frag), _lib.ptr(xs), _lib.ptr(corr), m_pad, _lib.ptr(flag), _lib.stream())
+    with pytest.raises(fq.ConfigError):
+        _lib.check(L.flexq_attn_block(*args, 64, *tail))
+    _lib.check(L.flexq_attn_block(*args, 128, *tail))
+    torch.cuda.synchronize()
+    assert int(flag.item()) & _lib.FLAG_KV_OVERFLOW
+    # nothing past the caches, nothing for the overflowing token; the in-range token appended
+    assert not kbuf[n:].any() and not vbuf[n:].any()
+    assert not kc[0].any() and kc[1, :, 1].any() and vc[1, :, 1].any()
+    with pytest.raises(fq.ConfigError):
+        FlexQLlamaDecoder(TINY, batch=1, max_len=8, group_size=64)
+    dec = FlexQLlamaDecoder(TINY, batch=1, max_len=2)
+    dec.step()
+    dec.step()
+    with pytest.raises(fq.InvalidInputError, match="KV cache full"):
+        dec.step()

@@ -96,6 +96,50 @@ def test_tc_llama13b_shapes(m, n, k, q):
     assert max_rel(y, y_ref) <= FP16_TOL
 
 
+LLAMA70B = {  # name: (N, K, q) -- the shapes the bench step serves (bench.py)
+    "qkv_proj": (10240, 8192, 6),
+    "o_proj": (8192, 8192, 6),
+    "gate_proj": (28672, 8192, 6),
+    "down_proj": (8192, 28672, 8),  # 224 k-blocks: deepest stream-K split
+}
+_CASES70 = {}
+
+
+def _case70(name, m):
+    key = (name, m)
+    if key not in _CASES70:
+        _CASES70.clear()  # one live case at a time: partials at M = 256 are ~2 GB
+        n, k, q = LLAMA70B[name]
+        _CASES70[key] = (n, k, case(m, n, k, q, 128, seed=m + n + k)[2:])
+    return _CASES70[key]
+
+
+@pytest.mark.parametrize("name", list(LLAMA70B))
+@pytest.mark.parametrize("m", [33, 64, 128, 256])
+@pytest.mark.parametrize("ksplit", [AUTO, TC])
+def test_tc_llama70b_shapes(name, m, ksplit):
+    """LLaMA-2-70B layers at the batches the tcgen05 route serves automatically (M > 32):
+    INT32 partials bit-exact against int_matmul_reference(trace=True) (engine.py:337-365),
+    fp16 y in tolerance, the automatic route identical to the forced tcgen05 route."""
+    n, k, (codes, y_ref, p_ref) = _case70(name, m)
+    y, parts = run(codes, m, n, k, 128, ksplit=ksplit)
+    assert np.array_equal(parts, p_ref)
+    del parts
+    assert max_rel(y, y_ref) <= FP16_TOL
+
+
+@pytest.mark.parametrize("name,m", [("gate_proj", 64), ("gate_proj", 128), ("down_proj", 64),
+                                    ("down_proj", 128)])
+def test_linear_llama70b_batched(name, m):
+    """FlexQLinear (fused quantizer -> tcgen05 GEMM, fp16 in/out) on the 70B layers."""
+    n, k, q = LLAMA70B[name]
+    w, x, _, y_ref, _ = case(m, n, k, q, 128, seed=5 * m + n)
+    lin = fq.FlexQLinear(w, activation_bits=q)
+    y = lin(torch.from_numpy(x).cuda()).float().cpu().numpy()
+    assert max_rel(y, y_ref) <= FP16_TOL
+    lin.check_errors()
+
+
 def test_tc_matches_mma_sync_kernel():
     m, n, k, q, gs = 80, 768, 3072, 8, 128
     _, _, codes, y_ref, p_ref = case(m, n, k, q, gs, seed=3)

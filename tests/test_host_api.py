@@ -74,6 +74,23 @@ def test_quanttensor_validation_host_arrays():  # test_quantize.py:117-138
     q = fq.QuantTensor(values=np.zeros((3, 300), np.int8), scales=np.ones((3, 3)), bits=6,
                        group_size=128)
     assert q.shape == (3, 300) and q.n_groups == 3
+    # wide integer codes are range-checked before any narrowing (65539 & 0xffff == 3)
+    with pytest.raises(fq.InvalidInputError):
+        fq.QuantTensor(values=np.full((1, 4), 65539, np.int32), scales=np.ones((1, 1)), bits=6,
+                       group_size=4)
+    torch = pytest.importorskip("torch")
+    with pytest.raises(fq.InvalidInputError):  # abs(int8 -128) wraps to -128 unless widened
+        fq.QuantTensor(values=torch.full((1, 4), -128, dtype=torch.int8),
+                       scales=torch.ones((1, 1), dtype=torch.float64), bits=8, group_size=4)
+
+
+def test_bit_planes_range_checked_before_narrowing():  # bitplane.py:60-64 (reference raises)
+    with pytest.raises(fq.InvalidInputError):
+        fq.bit_planes(np.array([[65539]], np.int32), 6)
+    with pytest.raises(fq.InvalidInputError):
+        fq.bit_planes(np.array([[-33, 0]], np.int64), 6)
+    with pytest.raises(fq.InvalidInputError):
+        fq.bit_planes(np.array([[64]], np.int16), 6, signed=False)
 
 
 def test_bmma_pass_accounting_matches_reference(golden):  # test_engine.py:243-271, test_bench.py:25-34
