@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--batch", type=int, default=1, help="tokens M per linear call")
-    ap.add_argument("--model", default="llama2-70b")
+    ap.add_argument("--model", default="llama2-70b",
+                    help="llama2-7b / llama2-13b / llama2-70b decoder-layer linears, or config1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--cpu-budget", type=float, default=2.0,
@@ -46,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bitserial", action="store_true",
                     help="also time the BTC-equivalent bit-serial kernel (extra key)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the M=8 and config-1 companion measurements")
     return ap.parse_args()
 
 
@@ -106,21 +109,55 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ---- reference arm: the reference's CPU path (oracle port) on host cores -------------------
+# ---- CPU baseline: the reference package itself when installed (baseline/_ref), else the port
+def cpu_baseline_impl():
+    from oracle import ref_baseline
+
+    if ref_baseline.available():
+        return ref_baseline.RefBaseline, ref_baseline.calibrate_rows, "reference"
+    from oracle.cpu_baseline import CpuBaseline, calibrate_rows
+
+    return CpuBaseline, calibrate_rows, "port"
+
+
+def reference_config1():
+    """BASELINE config 1 at full size through the reference's own call: 4096x4096 W6A8, M=1,
+    quantize + pack + group_matmul_fused (engine.py:290-334), one core (numpy), best of 3."""
+    import numpy as np
+
+    from oracle import ref_baseline
+
+    if not ref_baseline.available():
+        return None
+    lay = ref_baseline.RefLayer(4096, 4096, 8, np.random.default_rng(7), threads=1)
+    x = np.random.default_rng(8).standard_normal((1, 4096)).astype(np.float16).astype(np.float64)
+    best = min((time.perf_counter(), lay.run(x, None), time.perf_counter()) for _ in range(3))
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        lay.run(x, None)
+        ts.append(time.perf_counter() - t0)
+    del best
+    t = min(ts)
+    return {"workload": "config 1: single W6A8 4096x4096 linear, M=1, full size", "s_per_call": t,
+            "TOPS": 2 * 4096 * 4096 / t / 1e12, "cores": 1,
+            "path": "bitserial.quantize -> pack(decompose) -> group_matmul_fused (baseline/_ref)"}
+
+
+# ---- reference arm: the reference's CPU path on host cores --------------------------------------
 def run_reference(args, shapes, rank):
     if rank != 0:
         return
-    from oracle.cpu_baseline import CpuBaseline, calibrate_rows
-
+    Impl, calibrate_rows, kind = cpu_baseline_impl()
     threads = os.cpu_count() or 1
     budget = max(0.2, min(3.0, 120.0 / max(1, args.steps + args.warmup)))
     rows = calibrate_rows(shapes, args.batch, budget, threads)
-    cb = CpuBaseline(shapes, args.batch, rows, threads)
+    cb = Impl(shapes, args.batch, rows, threads)
     for _ in range(args.warmup):
         cb.step()
     t = sum(cb.step() for _ in range(args.steps))
     tops = cb.flops * args.steps / t / 1e12
-    print(json.dumps({
+    line = {
         "impl": "reference", "metric": METRIC, "value": tops, "unit": "TOPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -128,104 +165,67 @@ def run_reference(args, shapes, rank):
         "data": "synthetic fp16 N(0,1) weights/activations",
         "config": {"workload": f"{args.model} decoder-layer linears, M={args.batch}, sampled rows",
                    "batch": args.batch, "group_size": 128},
-        "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": threads, "kind": kind,
                          "sample": cb.describe()},
         "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }
+    if not args.no_extra:
+        line["config1"] = reference_config1()
+    print(json.dumps(line), flush=True)
 
 
 # ---- our arm ---------------------------------------------------------------------------------------
-def main():
-    args = parse()
-    import torch
+class Step:
+    """One bench step over `layers` at batch M: per linear the fused activation quantizer +
+    the T6 GEMV/GEMM (FlexQLinear.forward), then the shard-boundary collective under
+    torchrun; captured once in a CUDA graph.  `gemm` replays only the GEMM launches (the
+    dominant kernel, for the roofline)."""
 
-    from paper_2508_04405_b200.shapes import MODELS, gemm_bytes, layer_bytes, policy_kind
+    def __init__(self, torch, dist, layers, M, world, rank, dev):
+        self.torch, self.dist, self.layers, self.M, self.world = torch, dist, layers, M, world
+        self.dev = dev
+        self.inputs, self.x_loc, self.outs, self.gathered = {}, [], [], []
+        for s, lay in layers:
+            if s.k not in self.inputs:
+                gx = torch.Generator(device=dev)
+                gx.manual_seed(99 + s.k + 7919 * M)  # same activations on every rank
+                self.inputs[s.k] = torch.randn((M, s.k), generator=gx, device=dev, dtype=torch.float16)
+            kl = lay.k
+            self.x_loc.append(self.inputs[s.k][:, rank * kl:(rank + 1) * kl].contiguous()
+                              if lay.mode == "row" else self.inputs[s.k])
+            self.outs.append(torch.empty((M, lay.n), device=dev, dtype=torch.float32
+                                         if lay.mode == "row" else torch.float16))
+            self.gathered.append(torch.empty((world, M, lay.n), dtype=torch.float16, device=dev)
+                                 if world > 1 and lay.mode == "column" else None)
+        for _ in range(3):  # eager warm-up: allocates the per-M buffers
+            self.eager()
+        torch.cuda.synchronize()
+        self.graph, self.ggraph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(self.graph):
+                self.eager()
+            with torch.cuda.graph(self.ggraph):
+                self.gemm_eager()
+            self.run, self.gemm = self.graph.replay, self.ggraph.replay
+        except Exception as e:  # e.g. NCCL capture unsupported: time eager launches instead
+            print(f"[bench] graph capture failed ({e}); timing eager launches", file=sys.stderr)
+            self.run, self.gemm = self.eager, self.gemm_eager
 
-    shapes = MODELS[args.model]
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    def eager(self):
+        for i, (s, lay) in enumerate(self.layers):
+            lay.forward(self.x_loc[i], out=self.outs[i])
+            if self.world > 1:
+                if lay.mode == "row":
+                    self.dist.all_reduce(self.outs[i], op=self.dist.ReduceOp.SUM)
+                else:
+                    self.dist.all_gather_into_tensor(self.gathered[i], self.outs[i])
 
-    if args.impl == "reference":
-        run_reference(args, shapes, rank)
-        return
+    def gemm_eager(self):
+        for i, (s, lay) in enumerate(self.layers):
+            lay.gemm_only(self.M, self.outs[i])
 
-    import torch.distributed as dist
-
-    from paper_2508_04405_b200 import FlexQLinear
-
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    M = args.batch
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-
-    # Megatron pairing under torchrun (sharding.py): qkv/gate/up are
-    # column shards (rank r owns N/world output rows; replicated x; NCCL all-gather of the
-    # fp16 y shards), o/down are row shards (rank r owns K/world input columns on group
-    # boundaries; fp32 partial y; NCCL all-reduce).  world = 1: plain layers, no collective.
-    ROW_SHARDED = ("o_proj", "down_proj")
-    layers, inputs, outs, gathered, x_loc = [], {}, [], [], []
-    for s in shapes:
-        mode = "row" if (world > 1 and s.name in ROW_SHARDED) else "column"
-        n_loc, k_loc = (s.n, s.k // world) if mode == "row" else (s.n // world, s.k)
-        w = torch.randn((n_loc, k_loc), generator=g, device=dev, dtype=torch.float16)
-        lay = FlexQLinear(w, 6, s.act_bits, 128, fp16_scales=True, layer_kind=policy_kind(s.name))
-        lay.mode = mode
-        del w
-        layers.append((s, lay))
-        if s.k not in inputs:
-            gx = torch.Generator(device=dev)
-            gx.manual_seed(99 + s.k)  # same activations on every rank (replicated X)
-            inputs[s.k] = torch.randn((M, s.k), generator=gx, device=dev, dtype=torch.float16)
-        x_loc.append(inputs[s.k][:, rank * k_loc:(rank + 1) * k_loc].contiguous()
-                     if mode == "row" else inputs[s.k])
-        outs.append(torch.empty((M, n_loc), device=dev,
-                                dtype=torch.float32 if mode == "row" else torch.float16))
-        gathered.append(torch.empty((world, M, n_loc), dtype=torch.float16, device=dev)
-                        if world > 1 and mode == "column" else None)
-    torch.cuda.synchronize()
-
-    def collective(i, y):
-        if world == 1:
-            return
-        if layers[i][1].mode == "row":
-            dist.all_reduce(y, op=dist.ReduceOp.SUM)
-        else:
-            dist.all_gather_into_tensor(gathered[i], y)
-
-    def step():
-        for i, (s, lay) in enumerate(layers):
-            lay.forward(x_loc[i], out=outs[i])
-            collective(i, outs[i])
-
-    def gemm_step():
-        for i, (s, lay) in enumerate(layers):
-            lay.gemm_only(M, outs[i])
-
-    for _ in range(3):  # eager warm-up: allocates per-M buffers
-        step()
-    torch.cuda.synchronize()
-    graph, ggraph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-    use_graph = True
-    try:
-        with torch.cuda.graph(graph):
-            step()
-        with torch.cuda.graph(ggraph):
-            gemm_step()
-    except Exception as e:  # e.g. NCCL capture unsupported: time eager launches instead
-        print(f"[bench] graph capture failed ({e}); timing eager launches", file=sys.stderr)
-        use_graph = False
-    run = graph.replay if use_graph else step
-    run_gemm = ggraph.replay if use_graph else gemm_step
-
-    for _ in range(args.warmup):
-        run()
-    torch.cuda.synchronize()
-
-    def timed(fn, reps):
+    def timed(self, fn, reps):
+        torch, dist, world = self.torch, self.dist, self.world
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -239,16 +239,81 @@ def main():
             dist.barrier()
         ms = e0.elapsed_time(e1) / reps
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=self.dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
 
+    def summary(self, shapes, ms_step, ms_gemm):
+        from paper_2508_04405_b200.shapes import gemm_bytes
+
+        M = self.M
+        flops = sum(2 * M * s.n * s.k for s in shapes)
+        gb = sum(gemm_bytes(M, lay.n, lay.k) for _, lay in self.layers)
+        peak, _ = hbm_peak()
+        return {"ms_per_step": ms_step, "value": flops / (ms_step * 1e-3) / 1e12, "unit": "TOPS",
+                "gemm_us_per_step": ms_gemm * 1e3,
+                "roofline_frac": gb / (ms_gemm * 1e-3) / 1e9 / peak,
+                "step_frac": gb / (ms_step * 1e-3) / 1e9 / peak}
+
+
+def build_layers(torch, FlexQLinear, shapes, world, rank, dev, seed=1234):
+    """Random-init INT6 layers of the real shapes.  Megatron pairing under torchrun (SURVEY.md
+    sec. 8(e), sharding.py): qkv/gate/up are column shards (rank r owns N/world output rows;
+    replicated x; NCCL all-gather of the fp16 y shards), o/down are row shards (rank r owns
+    K/world input columns on group boundaries; fp32 partial y; NCCL all-reduce)."""
+    from paper_2508_04405_b200.shapes import policy_kind
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed + rank)
+    layers = []
+    for s in shapes:
+        mode = "row" if (world > 1 and s.name in ("o_proj", "down_proj")) else "column"
+        n_loc, k_loc = (s.n, s.k // world) if mode == "row" else (s.n // world, s.k)
+        w = torch.randn((n_loc, k_loc), generator=g, device=dev, dtype=torch.float16)
+        lay = FlexQLinear(w, 6, s.act_bits, 128, fp16_scales=True, layer_kind=policy_kind(s.name))
+        lay.mode = mode
+        del w
+        layers.append((s, lay))
+    torch.cuda.synchronize()
+    return layers
+
+
+def main():
+    args = parse()
+    import torch
+
+    from paper_2508_04405_b200.shapes import MODELS, WORKLOADS, layer_bytes
+
+    shapes = WORKLOADS.get(args.model) or MODELS[args.model]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, shapes, rank)
+        return
+
+    import torch.distributed as dist
+
+    from paper_2508_04405_b200 import FlexQLinear, _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    M = args.batch
+    layers = build_layers(torch, FlexQLinear, shapes, world, rank, dev)
+    st = Step(torch, dist, layers, M, world, rank, dev)
+    for _ in range(args.warmup):
+        st.run()
+    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ms_step = timed(run, args.steps)
-    ms_gemm = timed(run_gemm, max(args.steps // 2, 10))
+        ms_step = st.timed(st.run, args.steps)
+    ms_gemm = st.timed(st.gemm, max(args.steps // 2, 10))
 
     # ---- e2e through the public API: pinned host x -> device, one forward per layer, y -> pinned host
+    inputs = st.inputs
     host_in = {k: v.cpu().pin_memory() for k, v in inputs.items()}
     dev_in = {k: torch.empty_like(v) for k, v in inputs.items()}
     host_out = [torch.empty((M, s.n), dtype=torch.float16).pin_memory() for s, _ in layers]
@@ -284,20 +349,22 @@ def main():
             dev_in[k_].copy_(hv, non_blocking=True)
         for i, (s, lay) in enumerate(layers):
             if lay.mode == "row":
-                kl = s.k // world
+                kl = lay.k
                 y = lay(dev_in[s.k][:, rank * kl:(rank + 1) * kl].contiguous(),
                         out_dtype=torch.float32)
                 dist.all_reduce(y, op=dist.ReduceOp.SUM)
                 y = y.half()
             else:
                 y = lay(dev_in[s.k])
-                dist.all_gather_into_tensor(gathered[i], y)
-                y = gathered[i].permute(1, 0, 2).reshape(M, -1)
+                dist.all_gather_into_tensor(st.gathered[i], y)
+                y = st.gathered[i].permute(1, 0, 2).reshape(M, -1)
             host_out[i].copy_(y, non_blocking=True)
 
     for _ in range(5):
         e2e_step()
-    ms_e2e = timed(e2e_step, args.e2e_steps)
+    ms_e2e = st.timed(e2e_step, args.e2e_steps)
+
+    from paper_2508_04405_b200.shapes import gemm_bytes
 
     flops_total = sum(2 * M * s.n * s.k for s in shapes)  # whole job (all ranks)
     tops = flops_total / (ms_step * 1e-3) / 1e12
@@ -324,50 +391,86 @@ def main():
         f"{kern_gemv} + {kern_tc}"
     dtype_label = ("int8 IMMA mma.sync" if all(streamed) else "int8 tcgen05.mma kind::i8"
                    if not any(streamed) else "int8 IMMA mma.sync + tcgen05.mma kind::i8")
+    desc = (f"{args.model} decoder-layer linears qkv,o,gate,up (W6A6) + down (W6A8), M={M}"
+            if args.model in MODELS else WORKLOAD_DESC.get(args.model, args.model) + f", M={M}")
+    wbytes = sum(lay.weight_bytes for _, lay in layers) * world
     line = {
         "metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
         "dtype": dtype_label + " (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue, fp16 out",
         "data": "synthetic: random-init INT6 weights of the real shapes (fp16 N(0,1) quantized), fp16 N(0,1) activations",
-        "config": {"workload": f"{args.model} decoder-layer linears qkv,o,gate,up (W6A6) + down (W6A8), M={M}",
-                   "batch": M, "group_size": 128, "scales": "fp16",
+        "config": {"workload": desc, "batch": M, "group_size": 128, "scales": "fp16",
                    "parallelism": (f"tp{world}: qkv/gate/up column shards + NCCL all-gather, "
                                    f"o/down row shards (fp32 partials) + NCCL all-reduce")
                                   if world > 1 else "single GPU",
-                   "l2": "weights 642 MB/step > 126 MB L2 (no flush needed)",
+                   "l2": (f"weights {wbytes / 1e6:.0f} MB/step > 126 MB L2 (no flush needed)"
+                          if wbytes > 2 * 126e6 else
+                          f"weights {wbytes / 1e6:.0f} MB/step: L2 flushed between steps"),
                    "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks"},
         "latency_us_per_step": ms_step * 1e3,
-        "weight_GBps": sum(lay.weight_bytes for _, lay in layers) * world / (ms_step * 1e-3) / 1e9,
+        "weight_GBps": wbytes / (ms_step * 1e-3) / 1e9,
         "hbm_GBps_algorithmic": layer_b / (ms_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": kernel_label
                                + f" ({len(shapes)} launches/step, per-launch bytes in DESIGN.md sec. 4)",
-                     "peak_source": peak_kind, "gemm_us_per_step": ms_gemm * 1e3},
+                     "peak_source": peak_kind, "gemm_us_per_step": ms_gemm * 1e3,
+                     "step_frac": gbytes_loc / (ms_step * 1e-3) / 1e9 / peak},
         "clocks": clk.summary(),
         "e2e": {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TOPS",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": ms_e2e, "path": "FlexQLinear.__call__ (public API); per step one H2D of the inputs from pinned host memory and one D2H of all outputs"},
         "gpu_launches": args.steps * len(shapes) * launches_per_fwd,
     }
+    if world == 1 and not args.no_extra:
+        line["extra"] = extra_lines(torch, dist, FlexQLinear, layers, shapes, args, dev)
     if args.bitserial and world == 1:
         line["bitserial"] = time_bitserial(layers, M, shapes)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle.cpu_baseline import CpuBaseline, calibrate_rows
-
+        Impl, calibrate_rows, kind = cpu_baseline_impl()
         threads = os.cpu_count() or 1
         rows = calibrate_rows(shapes, M, args.cpu_budget, threads)
-        cb = CpuBaseline(shapes, M, rows, threads)
+        cb = Impl(shapes, M, rows, threads)
         cb.step()
         reps = 3
         tcpu = sum(cb.step() for _ in range(reps)) / reps
         line["cpu_baseline"] = {"value": cb.flops / tcpu / 1e12, "unit": "TOPS", "cores": threads,
-                                "kind": "port", "sample": cb.describe()}
+                                "kind": kind, "sample": cb.describe()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+WORKLOAD_DESC = {"config1": "BASELINE config 1: single W6A8 4096x4096 linear (GEMV)"}
+
+
+def extra_lines(torch, dist, FlexQLinear, layers, shapes, args, dev):
+    """Driver-run companions of the headline (same process, same clocks): the same 70B step
+    at M=8 (the top of the north star's batch 1-8 band) and BASELINE config 1 (one W6A8
+    4096x4096 linear at M=1; 12.6 MB of weights < L2, so 16 distinct copies are cycled to
+    stream from HBM)."""
+    from paper_2508_04405_b200.shapes import WORKLOADS
+
+    out = {}
+    if args.batch != 8 and args.model == "llama2-70b":
+        st = Step(torch, dist, layers, 8, 1, 0, dev)
+        for _ in range(20):
+            st.run()
+        out["llama2-70b_m8"] = st.summary(shapes, st.timed(st.run, 1000), st.timed(st.gemm, 500))
+        del st
+    c1 = WORKLOADS["config1"]
+    copies = [build_layers(torch, FlexQLinear, c1, 1, 0, dev, seed=4321 + i) for i in range(16)]
+    st = Step(torch, dist, [l for c in copies for l in c], 1, 1, 0, dev)  # 16 layers per replay
+    for _ in range(20):
+        st.run()
+    s16 = st.summary(c1 * 16, st.timed(st.run, 500), st.timed(st.gemm, 500))
+    s16["us_per_linear"] = s16["ms_per_step"] * 1e3 / 16
+    s16["gemm_us_per_linear"] = s16["gemm_us_per_step"] / 16
+    s16["note"] = "one replay = 16 distinct 4096x4096 W6A8 layers back to back (>2x L2 of weights)"
+    out["config1_w6a8_4096_m1"] = s16
+    return out
 
 
 def time_bitserial(layers, M, shapes):

@@ -15,9 +15,12 @@ class LinearShape:
     name: str   # layer kind (policy key)
     n: int
     k: int
+    bits: int = 0  # activation bits; 0 = the FlexQ policy for the layer kind
 
     @property
     def act_bits(self) -> int:
+        if self.bits:
+            return self.bits
         return 8 if self.name == "down_proj" else 6
 
 
@@ -37,6 +40,12 @@ MODELS = {
     "llama2-7b": _decoder(4096, 11008, 4096),
     "llama2-13b": _decoder(5120, 13824, 5120),
     "llama2-70b": _decoder(8192, 28672, 1024),  # GQA: 8 kv heads x 128
+}
+
+
+# single-linear workloads of BASELINE.json's config list
+WORKLOADS = {
+    "config1": [LinearShape("linear", 4096, 4096, bits=8)],  # config 1: W6A8 4096x4096, M=1
 }
 
 
