@@ -47,8 +47,6 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bitserial", action="store_true",
                     help="also time the BTC-equivalent bit-serial kernel (extra key)")
-    ap.add_argument("--no-chain", action="store_true",
-                    help="per-linear launches instead of one FlexQChain launch per step (M <= 16)")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the M=8 and config-1 companion measurements")
     return ap.parse_args()
@@ -183,18 +181,9 @@ class Step:
     torchrun; captured once in a CUDA graph.  `gemm` replays only the GEMM launches (the
     dominant kernel, for the roofline)."""
 
-    def __init__(self, torch, dist, layers, M, world, rank, dev, chain=True):
+    def __init__(self, torch, dist, layers, M, world, rank, dev):
         self.torch, self.dist, self.layers, self.M, self.world = torch, dist, layers, M, world
         self.dev = dev
-        # decode batches on one GPU: the step's linears as one FlexQChain launch (the same
-        # quantizer + GEMV arithmetic per linear, outputs identical to per-layer launches;
-        # csrc/gemv_chain.cu); under torchrun the shard-boundary collectives sit between
-        # the linears, so each linear is its own launch there
-        self.chain = None
-        if chain and world == 1 and M <= 16 and len(layers) <= 16:
-            from paper_2508_04405_b200 import FlexQChain
-
-            self.chain = FlexQChain([lay for _, lay in layers], depends_on_prev=True)
         self.inputs, self.x_loc, self.outs, self.gathered = {}, [], [], []
         for s, lay in layers:
             if s.k not in self.inputs:
@@ -223,9 +212,6 @@ class Step:
             self.run, self.gemm = self.eager, self.gemm_eager
 
     def eager(self):
-        if self.chain is not None:
-            self.chain(self.x_loc, outs=self.outs)
-            return
         for i, (s, lay) in enumerate(self.layers):
             lay.forward(self.x_loc[i], out=self.outs[i])
             if self.world > 1:
@@ -235,9 +221,6 @@ class Step:
                     self.dist.all_gather_into_tensor(self.gathered[i], self.outs[i])
 
     def gemm_eager(self):
-        if self.chain is not None:  # the chain kernel is the step's only launch
-            self.eager()
-            return
         for i, (s, lay) in enumerate(self.layers):
             lay.gemm_only(self.M, self.outs[i])
 
@@ -261,27 +244,17 @@ class Step:
             ms = float(t.item())
         return ms
 
-    def kernel_bytes(self):
-        """Algorithmic bytes of the dominant kernel(s) of one step: every GEMV's operands
-        (shapes.gemm_bytes); the chain kernel also reads each fp16 x and writes its operand."""
+    def summary(self, shapes, ms_step, ms_gemm):
         from paper_2508_04405_b200.shapes import gemm_bytes
 
         M = self.M
-        b = sum(gemm_bytes(M, lay.n, lay.k) for _, lay in self.layers)
-        if self.chain is not None:
-            b += sum(2 * M * lay.k + M * lay.k + 8 * M * (lay.k // 128) for _, lay in self.layers)
-        return b
-
-    def summary(self, shapes, ms_step, ms_gemm):
-        M = self.M
         flops = sum(2 * M * s.n * s.k for s in shapes)
-        gb = self.kernel_bytes()
+        gb = sum(gemm_bytes(M, lay.n, lay.k) for _, lay in self.layers)
         peak, _ = hbm_peak()
         return {"ms_per_step": ms_step, "value": flops / (ms_step * 1e-3) / 1e12, "unit": "TOPS",
                 "gemm_us_per_step": ms_gemm * 1e3,
                 "roofline_frac": gb / (ms_gemm * 1e-3) / 1e9 / peak,
-                "step_frac": gb / (ms_step * 1e-3) / 1e9 / peak,
-                "schedule": "chain" if self.chain is not None else "per-linear launches"}
+                "step_frac": gb / (ms_step * 1e-3) / 1e9 / peak}
 
 
 def build_layers(torch, FlexQLinear, shapes, world, rank, dev, seed=1234):
@@ -331,7 +304,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     M = args.batch
     layers = build_layers(torch, FlexQLinear, shapes, world, rank, dev)
-    st = Step(torch, dist, layers, M, world, rank, dev, chain=not args.no_chain)
+    st = Step(torch, dist, layers, M, world, rank, dev)
     for _ in range(args.warmup):
         st.run()
     torch.cuda.synchronize()
@@ -365,16 +338,11 @@ def main():
         out_views.append(dev_out_all[off:off + sz].view(M, lay.n))
         off += sz
 
-    chain_in = [in_views[s.k] for s, _ in layers]
-
     def e2e_step():
         if world == 1:
             dev_in_all.copy_(host_in_all, non_blocking=True)
-            if st.chain is not None:
-                st.chain(chain_in, outs=out_views)
-            else:
-                for i, (s, lay) in enumerate(layers):
-                    lay(in_views[s.k], out=out_views[i])
+            for i, (s, lay) in enumerate(layers):
+                lay(in_views[s.k], out=out_views[i])
             host_out_all.copy_(dev_out_all, non_blocking=True)
             return
         for k_, hv in host_in.items():
@@ -400,7 +368,7 @@ def main():
 
     flops_total = sum(2 * M * s.n * s.k for s in shapes)  # whole job (all ranks)
     tops = flops_total / (ms_step * 1e-3) / 1e12
-    gbytes_loc = st.kernel_bytes()
+    gbytes_loc = sum(gemm_bytes(M, lay.n, lay.k) for s, lay in layers)
     layer_b = sum(layer_bytes(M, s.n, s.k) for s in shapes)
     peak, peak_kind = hbm_peak()
     achieved = gbytes_loc / (ms_gemm * 1e-3) / 1e9
@@ -413,13 +381,11 @@ def main():
             traffic = prof["gemm_traffic_bytes_per_step"][key] / len(shapes)
     except Exception:
         pass
-    # per linear: fused activation quantizer + one GEMV/GEMM kernel; the chain: one launch
-    launches = args.steps * (1 if st.chain is not None else 2 * len(shapes))
+    launches_per_fwd = 2  # fused activation quantizer + one GEMV/GEMM kernel per linear
     # the automatic route (csrc/gemm_t6.cu): streaming GEMV for M <= 16, and for M <= 32 on
     # layers of >= 8192 units (64 rows x 128 k); tcgen05 otherwise
     streamed = [M <= 16 or (M <= 32 and -(-lay.n // 64) * -(-lay.k // 128) >= 8192) for _, lay in layers]
-    kern_gemv = ("flexq::gemv_chain_kernel (the step's linears in one persistent launch)"
-                 if st.chain is not None else "flexq::gemv_t6_stream_kernel")
+    kern_gemv = "flexq::gemv_t6_stream_kernel"
     kern_tc = "flexq::gemm_tc_kernel (tcgen05.mma kind::i8)"
     kernel_label = kern_gemv if all(streamed) else kern_tc if not any(streamed) else \
         f"{kern_gemv} + {kern_tc}"
@@ -441,26 +407,21 @@ def main():
                    "l2": (f"weights {wbytes / 1e6:.0f} MB/step > 126 MB L2 (no flush needed)"
                           if wbytes > 2 * 126e6 else
                           f"weights {wbytes / 1e6:.0f} MB/step: L2 flushed between steps"),
-                   "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks",
-                   "schedule": ("FlexQChain: quantizer + GEMV of every linear in one persistent "
-                                "launch, links ordered by grid barriers (each linear's x read "
-                                "after the previous linear's y is complete)")
-                               if st.chain is not None else "one quantizer + one GEMM launch per linear"},
+                   "timing": "CUDA-graph replay of the whole step, CUDA events, max over ranks"},
         "latency_us_per_step": ms_step * 1e3,
         "weight_GBps": wbytes / (ms_step * 1e-3) / 1e9,
         "hbm_GBps_algorithmic": layer_b / (ms_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": kernel_label
-                               + (" (1 launch/step" if st.chain is not None else f" ({len(shapes)} launches/step")
-                               + ", bytes per launch in DESIGN.md sec. 4)",
+                               + f" ({len(shapes)} launches/step, per-launch bytes in DESIGN.md sec. 4)",
                      "peak_source": peak_kind, "gemm_us_per_step": ms_gemm * 1e3,
                      "step_frac": gbytes_loc / (ms_step * 1e-3) / 1e9 / peak},
         "clocks": clk.summary(),
         "e2e": {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TOPS",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": ms_e2e, "path": "FlexQLinear.__call__ (public API); per step one H2D of the inputs from pinned host memory and one D2H of all outputs"},
-        "gpu_launches": launches,
+        "gpu_launches": args.steps * len(shapes) * launches_per_fwd,
     }
     if world == 1 and not args.no_extra:
         line["extra"] = extra_lines(torch, dist, FlexQLinear, layers, shapes, args, dev)
@@ -493,17 +454,12 @@ def extra_lines(torch, dist, FlexQLinear, layers, shapes, args, dev):
     from paper_2508_04405_b200.shapes import WORKLOADS
 
     out = {}
-    if args.model == "llama2-70b":
-        for m in (1, 8):
-            for chain in (True, False):
-                if m == args.batch and chain == (not args.no_chain):
-                    continue  # the headline itself
-                st = Step(torch, dist, layers, m, 1, 0, dev, chain=chain)
-                for _ in range(20):
-                    st.run()
-                key = f"llama2-70b_m{m}" + ("" if chain else "_per_linear_launches")
-                out[key] = st.summary(shapes, st.timed(st.run, 1000), st.timed(st.gemm, 500))
-                del st
+    if args.batch != 8 and args.model == "llama2-70b":
+        st = Step(torch, dist, layers, 8, 1, 0, dev)
+        for _ in range(20):
+            st.run()
+        out["llama2-70b_m8"] = st.summary(shapes, st.timed(st.run, 1000), st.timed(st.gemm, 500))
+        del st
     c1 = WORKLOADS["config1"]
     copies = [build_layers(torch, FlexQLinear, c1, 1, 0, dev, seed=4321 + i) for i in range(16)]
     st = Step(torch, dist, [l for c in copies for l in c], 1, 1, 0, dev)  # 16 layers per replay

@@ -182,34 +182,6 @@ int flexq_linear_forward_ex(const uint32_t* t6, const void* wscale, int scale_f1
                             void* y, int out_dtype, void* act_buf, void* workspace,
                             uint32_t* flag, const void* residual, cudaStream_t stream);
 
-/* ---- a chain of linears in one persistent launch (decode batches) ---------
- * Each link is one flexq_linear_forward (the online half of quantized_linear,
- * engine.py:487-513): quantize fp16 x [m, k] (quantize.py:118-148, fp16 scales) into
- * act_buf (flexq_act_buf_bytes(m, k, 128) bytes), then the T6 GEMV with the fused
- * group-dequant epilogue into fp16 y [m, n] (+ optional fp16 residual [m, n], may alias y).
- * The links run in order inside ONE persistent kernel (csrc/gemv_chain.cu): the next link's
- * weight stream starts during the current link's tail, and grid barriers order the phases
- * (depends_on_prev = 1: link i's x is read only after link i-1's y is complete).  Outputs
- * are identical to calling flexq_linear_forward per link.  Decode batches (1 <= m <= 16),
- * group_size 128, k a multiple of 128, at most 16 links; every link's weight scales use the
- * scale_f16 layout.  Data-dependent errors are OR-ed into *flag as for flexq_quantize. */
-typedef struct FlexQChainLink {
-  const uint32_t* t6;       /* flexq_pack_t6 weights [n, k]                   */
-  const void* wscale;       /* its scales (fp16 if scale_f16, else fp32)      */
-  const void* x;            /* fp16 activations [m, k], 8-byte aligned       */
-  void* act_buf;            /* flexq_act_buf_bytes(m, k, 128) bytes            */
-  void* y;                  /* fp16 output [m, n]                              */
-  const void* residual;     /* fp16 [m, n] added in the epilogue, or NULL      */
-  int64_t n, k, group_size; /* group_size must be 128                          */
-  int xbits;                /* activation bits (6 or 8 in FlexQ)               */
-  int depends_on_prev;      /* 1: read x only after the previous link's y      */
-} FlexQChainLink;
-int64_t flexq_chain_workspace_bytes(const FlexQChainLink* links, int n_links, int64_t m);
-/* workspace: flexq_chain_workspace_bytes(), zero-initialised once (left reusable). */
-int flexq_chain_forward(const FlexQChainLink* links, int n_links, int64_t m, int scale_f16,
-                        void* workspace, int64_t workspace_bytes, uint32_t* flag,
-                        cudaStream_t stream);
-
 /* ---- LLaMA-2 decode harness (BASELINE config 5) ---------
  * Producers and glue around the W6Ax linears for an end-to-end decode step.  The
  * reference has no model code; these are NOT part of its drop-in surface.

@@ -49,8 +49,6 @@ SIGNATURES = {
     "flexq_linear_forward": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, vp, vp, vp, vp]),
     "flexq_linear_forward_ex": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, i32, vp, vp, vp,
                                       vp, vp]),
-    "flexq_chain_workspace_bytes": (i64, [vp, i32, i64]),
-    "flexq_chain_forward": (i32, [vp, i32, i64, i32, vp, i64, vp, vp]),
     "flexq_rmsnorm_quantize": (i32, [vp, i64, vp, ctypes.c_float, i64, i64, i32, i64, vp, vp, vp,
                                      i64, vp, vp, vp]),
     "flexq_silu_mul_quantize": (i32, [vp, i64, i64, i64, i32, i64, vp, vp, vp, i64, vp, vp, vp]),
@@ -59,15 +57,6 @@ SIGNATURES = {
     "flexq_attn_block": (i32, [vp, vp, vp, vp, vp, i64, i32, i32, i64, ctypes.c_float, i32, i64,
                                vp, vp, vp, i64, vp, vp]),
 }
-
-
-
-class ChainLink(ctypes.Structure):
-    """struct FlexQChainLink (include/flexq.h)."""
-    _fields_ = [("t6", vp), ("wscale", vp), ("x", vp), ("act_buf", vp), ("y", vp),
-                ("residual", vp), ("n", i64), ("k", i64), ("group_size", i64), ("xbits", i32),
-                ("depends_on_prev", i32)]
-
 
 _lib = None
 _lock = threading.Lock()

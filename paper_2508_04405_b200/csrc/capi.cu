@@ -50,8 +50,6 @@ int attn_decode_launch(const void*, const void*, const void*, const int*, void*,
 int attn_block_launch(const void*, const int*, void*, void*, void*, int64_t, int, int, int64_t,
                       float, int, int64_t, uint32_t*, float*, int32_t*, int64_t, uint32_t*,
                       cudaStream_t);
-int64_t chain_workspace(const FlexQChainLink*, int, int64_t);
-int chain_launch(const FlexQChainLink*, int, int64_t, int, void*, int64_t, uint32_t*, cudaStream_t);
 int group_epilogue_launch(const int32_t*, const double*, const double*, int64_t, int64_t, int64_t,
                           double*, uint16_t*, cudaStream_t);
 
@@ -285,21 +283,6 @@ int flexq_linear_forward_ex(const uint32_t* t6, const void* wscale, int scale_f1
                             uint32_t* flag, const void* residual, cudaStream_t stream) {
   return linear_forward(t6, wscale, scale_f16, xbits, x, m, n, k, group_size, y, out_dtype,
                         act_buf, workspace, flag, residual, stream);
-}
-
-int64_t flexq_chain_workspace_bytes(const FlexQChainLink* links, int n_links, int64_t m) {
-  if (!links || n_links < 1) return 0;
-  return chain_workspace(links, n_links, m);
-}
-
-int flexq_chain_forward(const FlexQChainLink* links, int n_links, int64_t m, int scale_f16,
-                        void* workspace, int64_t workspace_bytes, uint32_t* flag,
-                        cudaStream_t stream) {
-  if (!links) {
-    set_error("chain_forward: links is NULL");
-    return FLEXQ_ERR_INVALID_INPUT;
-  }
-  return chain_launch(links, n_links, m, scale_f16, workspace, workspace_bytes, flag, stream);
 }
 
 /* ---- LLaMA decode harness (BASELINE config 5) ---- */

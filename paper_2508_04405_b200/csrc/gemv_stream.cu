@@ -593,11 +593,6 @@ static int stream_stages() {
   return s;
 }
 
-// When set, launch_stream_inst only plans: it writes the warp count the launch would use and
-// returns without launching (gemv_stream_plan_warps; the chain kernel splits every link over
-// exactly as many warps as the per-linear launch, so both give identical outputs).
-static thread_local int64_t* t_plan_nw = nullptr;
-
 template <int MT, int MODE, bool SF16, bool TRACE, bool FAST, int OUT, int S>
 static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
   auto kern = (MT == 1 && p.m == 1) ? gemv_t6_stream_kernel<MT, MODE, SF16, TRACE, FAST, OUT, S, MT == 1>
@@ -636,10 +631,6 @@ static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
   const int64_t by_units = cdiv(p.units, S >= 4 ? min_deep : kMinUnitsPerWarp);
   if (warps > by_units) warps = by_units;
   p.nw = warps;
-  if (t_plan_nw) {
-    *t_plan_nw = warps;
-    return FLEXQ_OK;
-  }
   const unsigned ctas = (unsigned)cdiv(warps, wpc);
   cudaError_t e = launch_pdl(kern, dim3(ctas), dim3(wpc * 32), (size_t)smem, st, p);
   if (e != cudaSuccess) return cuda_status(e, "gemv_t6_stream launch");
@@ -673,24 +664,6 @@ int64_t gemv_stream_workspace(int64_t m, int64_t n, int64_t k, int64_t gs) {
   T6Geom G(n, k, gs);
   const int64_t mt = m <= 8 ? 1 : m <= 16 ? 2 : 4;
   return cdiv(stream_slots(G.rg) * 4 * mt * 4 * 32 * 4, 256) * 256 + cdiv(G.rg * 4, 256) * 256;
-}
-
-int gemv_stream_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
-                       const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
-                       int, void*, const void*, cudaStream_t);
-
-// Warps the per-linear streaming launch splits an (n, k, gs) layer over at batch m (fast
-// path, fp16 out); -1 if the streaming kernel does not serve the shape.
-int64_t gemv_stream_plan_warps(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f16) {
-  int64_t nw = -1;
-  t_plan_nw = &nw;
-  static float dummy_y;
-  const int64_t m_pad = cdiv(m, kTokTile) * kTokTile;
-  const int rc = gemv_stream_launch(nullptr, nullptr, scale_f16, nullptr, nullptr, nullptr, m, m_pad,
-                                    n, k, gs, nullptr, &dummy_y, FLEXQ_OUT_F16,
-                                    reinterpret_cast<void*>(&dummy_y), nullptr, nullptr);
-  t_plan_nw = nullptr;
-  return rc == FLEXQ_OK ? nw : -1;
 }
 
 int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,

@@ -279,12 +279,36 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
   // room a persistent GEMM CTA launched behind it (PDL) needs on an SM
   auto quantize_item = [&](int64_t item, uint2 raw) {
     const int64_t r = item / ng, g = item - r * ng;
-    uint32_t word;
-    int csum;
-    const double sc = quantize_g128_lane(raw, A.bits, A.fp16_scales, A.flag, lane, word, csum);
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+    const double v[4] = {(double)f01.x, (double)f01.y, (double)f23.x, (double)f23.y};
+    bool finite = true;
+    float peak = 0.f;  // max of fp16 magnitudes: exact in fp32
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      finite &= isfinite(v[i]);
+      peak = fmaxf(peak, fabsf((float)v[i]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    if (!__all_sync(0xffffffffu, finite)) {
+      if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
+      peak = 0.f;
+    }
+    const double sc = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
+    int c[4], csum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      c[i] = code_of(v[i], sc, A.bits);
+      csum += c[i];
+    }
+    const uint32_t word = (uint32_t)(c[0] & 0xff) | ((uint32_t)(c[1] & 0xff) << 8) |
+                          ((uint32_t)(c[2] & 0xff) << 16) | ((uint32_t)(c[3] & 0xff) << 24);
     if (A.codes) *reinterpret_cast<uint32_t*>(A.codes + r * A.cols + g * 128 + lane * 4) = word;
     if (A.act_frag)
       *reinterpret_cast<uint32_t*>(A.act_frag + operand_word_offset(g, r, A.m_pad, lane)) = word;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
     if (lane == 0) {
       if (A.scales) A.scales[r * ng + g] = sc;
       if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)sc;

@@ -12,7 +12,7 @@ never allocates and can be captured in a CUDA graph.
 from __future__ import annotations
 
 from . import _dev, _lib
-from .errors import ConfigError, InvalidInputError, ShapeError
+from .errors import InvalidInputError, ShapeError
 from .packing import PackedTensor
 from .quantize import DEFAULT_GROUP_SIZE, DEFAULT_POLICY, BitPolicy, QuantTensor, quantize
 from .quantize import activation_bits as policy_bits
@@ -231,111 +231,6 @@ class FlexQLinear:
 
     def check_errors(self) -> None:
         """Raise if any forward since the last check saw non-finite input (host sync)."""
-        bits = int(self.flag.item())
-        self.flag.zero_()
-        if bits & _lib.FLAG_NONFINITE:
-            raise InvalidInputError("input contains non-finite values")
-        if bits & _lib.FLAG_NONPOS_SCALE:
-            raise InvalidInputError("all scales must be strictly positive")
-
-
-class FlexQChain:
-    """A sequence of FlexQLinear layers run as ONE persistent launch (flexq_chain_forward).
-
-    ``chain([x0, x1, ...])`` computes, in order, ``y_i = layers[i](x_i)`` -- the fused
-    activation quantizer and the T6 GEMV of every link, the same arithmetic as calling each
-    layer (outputs are identical) -- but inside a single kernel: the next layer's weight
-    stream starts during the current layer's tail and the quantizers run between grid
-    barriers instead of as separate launches (csrc/gemv_chain.cu).
-    With ``depends_on_prev`` (default) link i reads x_i only after link i-1's y is complete
-    (x_i may alias y_{i-1} when the shapes allow): the ordering of a stack of dependent
-    layers.  Without it the quantizer of link i runs as soon as link i-1's operand phase is
-    done (independent inputs, e.g. layers sharing one x).
-
-    Decode batches only (M <= 16), group size 128, K a multiple of 128, <= 16 links, all
-    layers with the same scale layout (fp16_scales) on one device.
-    """
-
-    MAX_LINKS = 16
-
-    def __init__(self, layers, depends_on_prev: bool = True):
-        layers = list(layers)
-        if not 1 <= len(layers) <= self.MAX_LINKS:
-            raise ConfigError(f"a chain holds 1..{self.MAX_LINKS} layers, got {len(layers)}")
-        dev = layers[0].device
-        for i, lay in enumerate(layers):
-            if not isinstance(lay, FlexQLinear):
-                raise InvalidInputError(f"link {i} is not a FlexQLinear")
-            if lay.group_size != 128 or lay.k % 128:
-                raise ConfigError(f"link {i}: the chain needs group_size 128 and K % 128 == 0 "
-                                  f"(got group {lay.group_size}, K={lay.k})")
-            if lay.device != dev or lay.fp16_scales != layers[0].fp16_scales:
-                raise ConfigError(f"link {i}: every link must share the device and scale layout")
-        if not depends_on_prev and len({id(l) for l in layers}) < len(layers):
-            # a repeated layer reuses its activation buffer: its next quantizer must wait
-            raise ConfigError("a layer repeated in a chain needs depends_on_prev=True")
-        self.layers = layers
-        self.device = dev
-        self.depends_on_prev = bool(depends_on_prev)
-        self.flag = _dev.torch().zeros(1, dtype=_dev.torch().int32, device=dev)
-        self._ws: dict = {}
-
-    def _workspace(self, m: int, links):
-        t = _dev.torch()
-        key = (m, _lib.stream())
-        if key not in self._ws:
-            if t.cuda.is_current_stream_capturing():
-                for (mm, _), ws in self._ws.items():
-                    if mm == m:
-                        return ws
-            nb = _lib.lib().flexq_chain_workspace_bytes(links, len(self.layers), m)
-            self._ws[key] = t.zeros(nb, dtype=t.uint8, device=self.device)
-        return self._ws[key]
-
-    def forward(self, xs, outs=None, residuals=None):
-        """xs: one fp16 CUDA [M, K_i] per link -> list of fp16 [M, N_i] (no host sync).
-        ``residuals[i]`` (fp16 [M, N_i], may be ``outs[i]``) is added in link i's epilogue."""
-        t = _dev.torch()
-        n = len(self.layers)
-        if len(xs) != n:
-            raise ShapeError(f"chain of {n} links got {len(xs)} inputs")
-        m = int(xs[0].shape[0]) if xs[0].dim() == 2 else -1
-        if not 1 <= m <= 16:
-            raise ShapeError(f"the chain serves decode batches 1..16, got M={m}")
-        outs = list(outs) if outs is not None else [None] * n
-        residuals = list(residuals) if residuals is not None else [None] * n
-        links = (_lib.ChainLink * n)()
-        keep = []
-        for i, (lay, x) in enumerate(zip(self.layers, xs)):
-            if not _dev.is_torch(x) or x.dim() != 2 or tuple(x.shape) != (m, lay.k):
-                raise ShapeError(f"link {i}: activation shape {tuple(getattr(x, 'shape', ()))} "
-                                 f"!= ({m}, {lay.k})")
-            if not x.is_cuda or x.device != self.device:
-                raise InvalidInputError(f"link {i}: x must be a CUDA tensor on {self.device}")
-            if x.dtype != t.float16 or not x.is_contiguous() or x.data_ptr() % 8:
-                x = x.to(t.float16).contiguous()
-                keep.append(x)
-            if outs[i] is None:
-                outs[i] = t.empty((m, lay.n), dtype=t.float16, device=self.device)
-            else:
-                lay._check_out("out", outs[i], m, t.float16)
-            if residuals[i] is not None:
-                lay._check_out("residual", residuals[i], m, t.float16)
-            act, _ = lay.buffers(m)
-            links[i] = _lib.ChainLink(lay.t6.data_ptr(), lay.wscale.data_ptr(), x.data_ptr(),
-                                      act.data_ptr(), outs[i].data_ptr(),
-                                      _lib.ptr(residuals[i]), lay.n, lay.k, 128,
-                                      lay.activation_bits, int(self.depends_on_prev))
-        ws = self._workspace(m, links)
-        _lib.check(_lib.lib().flexq_chain_forward(links, n, m, int(self.layers[0].fp16_scales),
-                                                  ws.data_ptr(), ws.numel(), self.flag.data_ptr(),
-                                                  _lib.stream()))
-        return outs
-
-    __call__ = forward
-
-    def check_errors(self) -> None:
-        """Raise if any chain call since the last check saw non-finite input (host sync)."""
         bits = int(self.flag.item())
         self.flag.zero_()
         if bits & _lib.FLAG_NONFINITE:

@@ -1,3 +1,12 @@
+// EXPERIMENT (not built into libflexq_sm100a.so) -- kept with its measurement, DESIGN.md sec. 4.1.
+// Round 2: the five LLaMA-2-70B decode linears as one persistent "chain" launch (grid
+// barriers between links, next-link weight prefetch during the tail) were bit-identical to
+// per-linear launches but SLOWER: 174 us vs 143.7 us per M=1 step (profiles/
+// r02_bench_chain_experiment.json).  The per-CTA timeline (profiles/r02_chain_timeline.txt,
+// tools/experiments/chain_timeline.py) shows why: each grid barrier costs ~2 us (444
+// same-address arrivals serialise in L2) and the in-kernel quantizer phase ~2.5 us, so a
+// link boundary costs ~7 us -- more than the ~2.8 us a PDL-overlapped per-linear launch pays.
+// It compiled against an older C ABI (FlexQChainLink in flexq.h), which was removed with it.
 // A chain of decode-regime W6Ax linears in ONE persistent launch (M <= 16, group 128).
 //
 // Each link is the online half of the reference's quantized_linear (engine.py:487-513):
@@ -56,7 +65,10 @@ struct ChainParams {
   unsigned* counters;  // per row group (max over links), zero between links
   unsigned* gbar;      // [0] arrival counter, [32] epoch (own 128 B lines)
   uint32_t* flag;
+  long long* tl;       // debug timeline (FLEXQ_CHAIN_TIMELINE), normally NULL:
+                       // per CTA [start, then per link: barrier A in/out, B out, loop done]
 };
+constexpr int kChainTlPerCta = 1 + 4 * kChainMax;
 
 template <int MT, bool SF16>
 struct ChainStage {
@@ -226,12 +238,18 @@ __global__ void __launch_bounds__(kChainWarps * 32) gemv_chain_kernel(const __gr
       for (int i = 0; i < S && u0 + i < u1; i++) issue(l, u0 + i, (s + i) % S, 0);
     pro = (int)(u1 - u0 < S ? u1 - u0 : S);
   };
+  auto mark = [&](int slot) {
+    if (p.tl && threadIdx.x == 0) p.tl[blockIdx.x * kChainTlPerCta + slot] = dbg_now();
+  };
+  mark(0);
   prefetch_weights(p.L[0]);
   pdl_wait();
 
   for (int j = 0; j < p.nl; j++) {
     const ChainLinkDev& l = p.L[j];
+    mark(1 + 4 * j);
     if (j > 0 && l.dep) grid_barrier(p.gbar, gridDim.x);  // y_{j-1} complete
+    mark(2 + 4 * j);
     // ---- quantizer phase: (row, group) items of x_j over all warps of the grid ----
     {
       const int64_t ng = l.kb, items = m * ng;
@@ -250,6 +268,7 @@ __global__ void __launch_bounds__(kChainWarps * 32) gemv_chain_kernel(const __gr
       asm volatile("fence.proxy.async.global;" ::: "memory");  // read back by TMA after B
     }
     grid_barrier(p.gbar, gridDim.x);  // x_j's operand complete
+    mark(3 + 4 * j);
     if (j == p.nl - 1) pdl_launch_dependents();
     if (gw < l.nw) {
       const int64_t u0 = gw * l.units / l.nw, u1 = (gw + 1) * l.units / l.nw;
@@ -345,6 +364,11 @@ __global__ void __launch_bounds__(kChainWarps * 32) gemv_chain_kernel(const __gr
       }
       if (kb != 0) flush(l, rg, gw);
     }
+    __syncwarp();
+    if (p.tl) {  // (debug) CTA-level loop end = its slowest warp
+      __syncthreads();
+      mark(4 + 4 * j);
+    }
     // the next link's weight stream starts now, during this link's tail
     if (j + 1 < p.nl) prefetch_weights(p.L[j + 1]);
   }
@@ -352,6 +376,15 @@ __global__ void __launch_bounds__(kChainWarps * 32) gemv_chain_kernel(const __gr
 
 // ---- host side ------------------------------------------------------------------------------
 int64_t gemv_stream_plan_warps(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f16);
+static long long* g_chain_tl = nullptr;
+static int g_chain_ctas = 0;
+extern "C" int flexq_debug_chain_timeline(long long* host, int max_entries) {
+  const int n = g_chain_ctas * kChainTlPerCta;
+  if (!g_chain_tl || max_entries < n) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_chain_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
+  return g_chain_ctas;
+}
 
 int64_t chain_workspace(const FlexQChainLink* links, int nl, int64_t m) {
   int64_t rg_max = 0;
@@ -392,6 +425,7 @@ static int chain_launch_inst(ChainParams& p, int dev, cudaStream_t st) {
   }
   if (per_sm > 4) per_sm = 4;  // fixup slots are sized for <= 16 warps per SM
   const int ctas = c.sms * per_sm;
+  g_chain_ctas = ctas;
   p.tw = (int64_t)ctas * kChainWarps;
   for (int i = 0; i < p.nl; i++) {
     ChainLinkDev& l = p.L[i];
@@ -495,6 +529,13 @@ int chain_launch(const FlexQChainLink* links, int nl, int64_t m, int scale_f16, 
   p.counters = reinterpret_cast<unsigned*>(ws + slot_bytes);
   p.gbar = reinterpret_cast<unsigned*>(ws + slot_bytes + cdiv(rg_max * 4, 256) * 256);
   p.flag = flag;
+  static long long* tlbuf = nullptr;
+  if (getenv("FLEXQ_CHAIN_TIMELINE")) {  // debug only (tools/chain_timeline.py)
+    if (!tlbuf) cudaMalloc(&tlbuf, 148 * 16 * kChainTlPerCta * sizeof(long long));
+    cudaMemsetAsync(tlbuf, 0, 148 * 16 * kChainTlPerCta * sizeof(long long), st);
+    p.tl = tlbuf;
+    g_chain_tl = tlbuf;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   const bool sf16 = scale_f16 != 0;
