@@ -205,6 +205,7 @@ struct TcParams {
 
 // timeline record: [role][unit][event] clock64 stamps for CTA 0
 constexpr int kTlUnits = 64;
+constexpr int kTlRoles = 6;  // converters, MMA, epilogue x2, weight producer, B/slot producer
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -212,7 +213,7 @@ __device__ __forceinline__ long long gtimer() {
 }
 // per-CTA wall marks (ns): [0] start, [1] MMA loop done, [2] epilogue done, [3] units
 __device__ __forceinline__ void cta_mark(const TcParams& p, int ev, long long v) {
-  if (p.trace_clk) p.trace_clk[4 * kTlUnits * 4 + blockIdx.x * 4 + ev] = v;
+  if (p.trace_clk) p.trace_clk[kTlRoles * kTlUnits * 4 + blockIdx.x * 4 + ev] = v;
 }
 __device__ __forceinline__ void tl_mark(const TcParams& p, int role, int64_t i, int ev) {
   if (p.trace_clk && blockIdx.x == 0 && i < kTlUnits)
@@ -381,13 +382,16 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
         const int rg0 = c.rt * 2;
         const int nu = rg0 + 1 < p.rg ? 2 : 1;
+        tl_mark(p, 4, c.u - u0, 0);
         mbar_wait(&wempty[wi], wph ^ 1u);
+        tl_mark(p, 4, c.u - u0, 1);
         mbar_expect_tx(&wfull[wi], nu * kUnitBytes);
         uint8_t* dst = smem + C::kOffRaw + wi * C::kRaw;
         bulk_g2s(dst, p.t6 + ((int64_t)rg0 * kbn + c.kb) * kUnitBytes, kUnitBytes, &wfull[wi], pol);
         if (nu == 2)
           bulk_g2s(dst + kUnitBytes, p.t6 + ((int64_t)(rg0 + 1) * kbn + c.kb) * kUnitBytes,
                    kUnitBytes, &wfull[wi], pol);
+        tl_mark(p, 4, c.u - u0, 2);
         if (++wi == C::SW) { wi = 0; wph ^= 1u; }
       }
     }
@@ -402,12 +406,15 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
       int bi = 0, si = 0;
       uint32_t bph = 0, sph = 0;
       for (TcCursor c(p, u0, u1); c.valid(); c.next(p)) {
+        tl_mark(p, 5, c.u - u0, 0);
         mbar_wait(&aempty[bi], bph ^ 1u);
+        tl_mark(p, 5, c.u - u0, 1);
         mbar_expect_tx(&afull[bi], C::kB);
         bulk_g2s(smem + C::kOffB + bi * C::kB,
                  p.act + ((int64_t)c.kb * (p.m_pad >> 3) + (int64_t)c.tt * (TN / 8)) * 1024, C::kB,
                  &afull[bi], pol);
         if (++bi == C::SA) { bi = 0; bph ^= 1u; }
+        tl_mark(p, 5, c.u - u0, 2);
         if (!c.drain_end(p)) continue;
         mbar_wait(&sempty[si], sph ^ 1u);
         const int rg0 = c.rt * 2;
@@ -424,6 +431,7 @@ __global__ void __launch_bounds__(TcCfg<TN>::kThreads, 1) gemm_tc_kernel(TcParam
                          p.geo.scale_index((int64_t)(rg0 + r) * kRowGroup, c.g, 0) * (swb / 32),
                      swb, &sfull[si], pol);
         }
+        tl_mark(p, 5, c.u - u0, 3);
         if (++si == C::SS) { si = 0; sph ^= 1u; }
       }
     }
@@ -955,7 +963,7 @@ static int dispatch_tc(const TcParams& p, bool sf16, bool trace, bool fast, int 
 // debug: copy CTA 0's last timeline to host (FLEXQ_TC_TIMELINE set); returns entries
 static long long* g_tl = nullptr;
 extern "C" int flexq_debug_tc_timeline(long long* host, int max_entries) {
-  const int n = 4 * kTlUnits * 4 + 4 * 1024;
+  const int n = kTlRoles * kTlUnits * 4 + 4 * 1024;
   if (!g_tl || max_entries < n) return 0;
   cudaDeviceSynchronize();
   cudaMemcpy(host, g_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -998,8 +1006,8 @@ int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const 
   p.res = residual;
   if (getenv("FLEXQ_TC_DBG")) p.dbg = atoi(getenv("FLEXQ_TC_DBG"));
   if (getenv("FLEXQ_TC_TIMELINE")) {
-    if (!g_tl) cudaMalloc(&g_tl, (4 * kTlUnits * 4 + 4 * 1024) * sizeof(long long));
-    cudaMemsetAsync(g_tl, 0, (4 * kTlUnits * 4 + 4 * 1024) * sizeof(long long), st);
+    if (!g_tl) cudaMalloc(&g_tl, (kTlRoles * kTlUnits * 4 + 4 * 1024) * sizeof(long long));
+    cudaMemsetAsync(g_tl, 0, (kTlRoles * kTlUnits * 4 + 4 * 1024) * sizeof(long long), st);
     p.trace_clk = g_tl;
   }
   if (workspace) {

@@ -15,6 +15,9 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t a) {
 __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
   asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc) : "memory");
 }
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc) : "memory");
+}
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar)) : "memory");
 }
@@ -53,7 +56,9 @@ __global__ void probe(long long* out, int iters, int mode) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = holder;
-  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t idesc = (mode & 128)
+      ? (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24)   // bf16 x bf16 -> f32
+      : (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);  // u8 x s8 -> s32
   if (threadIdx.x == 0) {
     long long t0 = clock64();
     uint32_t ph = 0;
@@ -61,7 +66,10 @@ __global__ void probe(long long* out, int iters, int mode) {
       const int st = it & 3;
       const uint64_t ad = (mode & 1) ? desc_sw128(s32(A + st * 16384)) : desc_none(s32(A + st * 16384));
       const uint64_t bd = desc_none(s32(B + st * N * 128));
-      if (mode & 96) {  // interleave C independent accumulator chains (k-blocks to distinct D)
+      if (mode & 128) {  // kind::f16 (bf16): K=16 per instruction = 32 B, same byte steps as i8
+        const int nk = (mode & 256) ? 4 : 8;  // 4: half a 128-k block (same bytes as 4 x i8)
+        for (int s = 0; s < nk; s++) mma_f16(tmem + (it & 1) * N, ad + (s & 3) * 2, bd + (s & 3) * 16, idesc);
+      } else if (mode & 96) {  // interleave C independent accumulator chains (k-blocks to distinct D)
         const int C = (mode & 32) ? 2 : 4;
         for (int s = 0; s < 4; s++)
           for (int j = 0; j < C; j++)
@@ -101,7 +109,13 @@ void run(long long* d) {
                       "", "A sw128 + kernel-shaped sync", "", "", "", "A sw128 + commit only", "", "", "", "", "", "",
                       "A TMEM", "", "", "", "A TMEM + kernel-shaped sync", "", "", "", "A TMEM + commit only", "", "", "", "", "", "", "", "", "2 chains", "", "", "", "", "", "", "", "", "", "", "", "", "", "", "",
                       "", "", "", "", "", "", "", "", "", "", "", "", "", "", "", "", "4 chains", "", "", "", "4 chains + sync"};
-  for (int mode : {1, 5, 16, 33, 65, 65 + 4}) {
+  auto name = [&](int mode) -> const char* {
+    if (mode == 129) return "bf16 kind::f16, 8 x K=16";
+    if (mode == 133) return "bf16 kind::f16 8x + sync";
+    if (mode == 385) return "bf16 kind::f16, 4 x K=16";
+    return mn[mode];
+  };
+  for (int mode : {1, 5, 16, 33, 65, 65 + 4, 129, 129 + 4, 129 + 256}) {
     if (N > 128 && (mode & 16)) continue;
     if (N > 128 && (mode & 64)) continue;
     const int iters = 2000;
@@ -110,8 +124,8 @@ void run(long long* d) {
     if (e) { printf("err %s\n", cudaGetErrorString(e)); return; }
     long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     double cyc = (double)h / iters;
-    double ops = 2.0 * 128 * N * 128;
-    printf("N=%3d %-30s %7.1f cycles/k-block  %6.0f ops/clk/SM (peak ~15500)\n", N, mn[mode], cyc, ops / cyc);
+    double ops = 2.0 * 128 * N * (mode == 385 ? 64 : 128);
+    printf("N=%3d %-30s %7.1f cycles/k-block  %6.0f ops/clk/SM (peak ~15500)\n", N, name(mode), cyc, ops / cyc);
   }
 }
 
