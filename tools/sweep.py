@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--ms", default="1,2,4,8,16,32,64,128,256")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--no-mma", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true",
+                    help="skip the cuBLAS fp16 (W16A16) and cuBLASLt int8 (W8A8) comparators")
     args = ap.parse_args()
 
     import torch
@@ -55,6 +57,8 @@ def main():
     ms = [int(v) for v in args.ms.split(",")]
 
     def timed(fn, reps):
+        fn()  # eager warm-up (library handles, workspaces) before the capture
+        torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             fn()
@@ -129,6 +133,41 @@ def main():
                 row["tops_mma_sync"] = 2 * m * s.n * s.k / (row["us_mma_sync"] * 1e-6) / 1e12
             print(json.dumps(row), flush=True)
         del lays, base
+        torch.cuda.empty_cache()
+        if args.no_cublas:
+            continue
+        # external comparators on the same layer (the paper's baseline is cuBLAS W8A8,
+        # PAPER.md:498,511): torch.matmul fp16 -> cuBLAS, torch._int_mm int8 -> cuBLASLt,
+        # weights rotated over >= 2x L2 like ours; activations already in the GEMM's dtype
+        w16 = [torch.randn((s.n, s.k), device=dev, dtype=torch.float16)
+               for _ in range(max(1, -(-2 * L2_BYTES // (s.n * s.k * 2))))]
+        w8 = [torch.randint(-127, 128, (s.k, s.n), device=dev, dtype=torch.int8).t().contiguous().t()
+              for _ in range(max(1, -(-2 * L2_BYTES // (s.n * s.k))))]
+        for m in ms:
+            row = {"model": args.model, "layer": s.name, "m": m, "n": s.n, "k": s.k,
+                   "comparator": "cuBLAS"}
+            x16 = torch.randn((m, s.k), device=dev, dtype=torch.float16)
+            o16 = [torch.empty((m, s.n), device=dev, dtype=torch.float16) for _ in w16]
+
+            def f16():
+                for w_, o_ in zip(w16, o16):
+                    torch.matmul(x16, w_.t(), out=o_)
+
+            row["us_cublas_f16"] = timed(f16, args.reps) / len(w16) * 1e3
+            if m > 16 and m % 8 == 0:  # torch._int_mm: M > 16, multiples of 8
+                x8 = torch.randint(-127, 128, (m, s.k), device=dev, dtype=torch.int8)
+                o8 = [torch.empty((m, s.n), device=dev, dtype=torch.int32) for _ in w8]
+
+                def i8():
+                    for w_, o_ in zip(w8, o8):
+                        torch._int_mm(x8, w_, out=o_)
+
+                try:
+                    row["us_cublas_i8"] = timed(i8, args.reps) / len(w8) * 1e3
+                except Exception as e:  # pragma: no cover
+                    row["us_cublas_i8_error"] = str(e)[:80]
+            print(json.dumps(row), flush=True)
+        del w16, w8
         torch.cuda.empty_cache()
 
 
