@@ -422,6 +422,7 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": ms_e2e, "path": "FlexQLinear.__call__ (public API); per step one H2D of the inputs from pinned host memory and one D2H of all outputs"},
         "gpu_launches": args.steps * len(shapes) * launches_per_fwd,
+        "tuning": _lib.lib().flexq_tuning().decode(),
     }
     if world == 1 and not args.no_extra:
         line["extra"] = extra_lines(torch, dist, FlexQLinear, layers, shapes, args, dev)

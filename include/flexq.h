@@ -50,6 +50,9 @@ extern "C" {
 #define FLEXQ_OUT_F32 1
 
 const char* flexq_last_error(void);
+/* The FLEXQ_* debug / A-B environment knobs in effect ("defaults" when none is set); they
+ * are read once, at the library's first use, never per launch. */
+const char* flexq_tuning(void);
 int flexq_version(void);                  /* MAJOR*10000 + MINOR*100 + PATCH */
 int flexq_device_check(void);             /* 0 if an sm_100 device is current, else FLEXQ_ERR_CUDA */
 

@@ -27,6 +27,7 @@ i64, i32, vp, cstr = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_cha
 # name -> (restype, argtypes); every symbol declared in include/flexq.h
 SIGNATURES = {
     "flexq_last_error": (cstr, []),
+    "flexq_tuning": (cstr, []),
     "flexq_version": (i32, []),
     "flexq_device_check": (i32, []),
     "flexq_quantize": (i32, [vp, i32, i64, i64, i32, i64, i32, vp, vp, vp, vp, vp, i64, vp, vp]),

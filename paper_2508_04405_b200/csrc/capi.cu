@@ -3,6 +3,11 @@
 // Python wrapper can map status codes to the same exception classes.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -61,9 +66,64 @@ static int check_chunk_m(int cm) {
   return FLEXQ_OK;
 }
 
+// ---- runtime: knobs read once, per-device caches -----------------------------------------
+static const char* env(const char* name) { return getenv(name); }
+
+const Tuning& tuning() {
+  static const Tuning t = [] {
+    Tuning v;
+    v.trace = env("FLEXQ_TRACE") != nullptr;
+    v.disable_tc = env("FLEXQ_DISABLE_TC") && atoi(env("FLEXQ_DISABLE_TC")) == 1;
+    v.gemv_wide = env("FLEXQ_GEMV_WIDE") != nullptr;
+    v.gemv_rev = env("FLEXQ_GEMV_REV") != nullptr;
+    v.gemv_timeline = env("FLEXQ_GEMV_TIMELINE") != nullptr;
+    v.tc_timeline = env("FLEXQ_TC_TIMELINE") != nullptr;
+    v.q_early = env("FLEXQ_Q_EARLY") != nullptr;
+    if (env("FLEXQ_STREAM_MAX_M") && atoi(env("FLEXQ_STREAM_MAX_M")) >= 1)
+      v.stream_max_m = atoi(env("FLEXQ_STREAM_MAX_M"));
+    if (env("FLEXQ_STREAM_STAGES")) {
+      const int k = atoi(env("FLEXQ_STREAM_STAGES"));
+      if (k >= 2 && k <= 4) v.stream_stages = k;
+    }
+    if (env("FLEXQ_MIN_UNITS") && atoi(env("FLEXQ_MIN_UNITS")) > 0)
+      v.min_units = atoi(env("FLEXQ_MIN_UNITS"));
+    return v;
+  }();
+  return t;
+}
+
+static std::mutex g_rt_mu;
+constexpr int kMaxDevices = 64;
+
+int device_sms() {
+  static int sms[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
+  }
+  return sms[dev];
+}
+
+cudaError_t ensure_smem(const void* kern, int bytes) {
+  struct Entry { int dev; const void* kern; int bytes; };
+  static std::vector<Entry> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_rt_mu);
+  for (const Entry& e : done)
+    if (e.dev == dev && e.kern == kern && e.bytes >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back({dev, kern, bytes});
+  return e;
+}
+
 long long* dbg_trace_buf() {
   static long long* buf = nullptr;
-  static const bool on = getenv("FLEXQ_TRACE") != nullptr;
+  static const bool on = tuning().trace;
   if (on && !buf) {
     cudaMalloc(&buf, (4 + 4 * kDbgCap) * sizeof(long long));
     cudaMemset(buf, 0, 4 * sizeof(long long));
@@ -97,6 +157,29 @@ extern "C" int flexq_debug_trace(long long* host, int max_records) {
 extern "C" {
 
 const char* flexq_last_error(void) { return g_err; }
+
+const char* flexq_tuning(void) {
+  static std::string desc;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const Tuning& t = tuning();
+    const Tuning d;
+    std::string s;
+    auto add = [&](const char* k, const std::string& v) { s += (s.empty() ? "" : ",") + std::string(k) + "=" + v; };
+    if (t.trace != d.trace) add("FLEXQ_TRACE", "1");
+    if (t.disable_tc != d.disable_tc) add("FLEXQ_DISABLE_TC", "1");
+    if (t.gemv_wide != d.gemv_wide) add("FLEXQ_GEMV_WIDE", "1");
+    if (t.gemv_rev != d.gemv_rev) add("FLEXQ_GEMV_REV", "1");
+    if (t.gemv_timeline != d.gemv_timeline) add("FLEXQ_GEMV_TIMELINE", "1");
+    if (t.tc_timeline != d.tc_timeline) add("FLEXQ_TC_TIMELINE", "1");
+    if (t.q_early != d.q_early) add("FLEXQ_Q_EARLY", "1");
+    if (t.stream_max_m != d.stream_max_m) add("FLEXQ_STREAM_MAX_M", std::to_string(t.stream_max_m));
+    if (t.stream_stages != d.stream_stages) add("FLEXQ_STREAM_STAGES", std::to_string(t.stream_stages));
+    if (t.min_units != d.min_units) add("FLEXQ_MIN_UNITS", std::to_string(t.min_units));
+    desc = s.empty() ? "defaults" : s;
+  });
+  return desc.c_str();
+}
 
 int flexq_version(void) { return 100; /* 0.1.0 */ }
 

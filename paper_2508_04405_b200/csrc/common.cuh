@@ -19,6 +19,28 @@ int cuda_status(cudaError_t e, const char* where);
     if (_e != cudaSuccess) return ::flexq::cuda_status(_e, where); \
   } while (0)
 
+// ---- runtime (host): environment knobs, per-device caches ----------------------
+// Every FLEXQ_* environment knob is read ONCE, at the library's first use (tuning()); the
+// values are reported by flexq_tuning() so a benchmark line can record them.  The product
+// path never reads the environment per launch.  The knobs are debug / A-B switches only;
+// unset, the automatic routes documented in DESIGN.md sec. 4 apply.
+struct Tuning {
+  bool trace = false;          // FLEXQ_TRACE: kernel event trace (tools/step_trace.py)
+  bool disable_tc = false;     // FLEXQ_DISABLE_TC=1: M > 16 on the mma.sync kernel
+  bool gemv_wide = false;      // FLEXQ_GEMV_WIDE: one 12-warp GEMV CTA per SM
+  bool gemv_rev = false;       // FLEXQ_GEMV_REV: reversed unit-range assignment
+  bool gemv_timeline = false;  // FLEXQ_GEMV_TIMELINE: per-warp GEMV timeline
+  bool tc_timeline = false;    // FLEXQ_TC_TIMELINE: tcgen05 CTA-0 timeline
+  bool q_early = false;        // FLEXQ_Q_EARLY: quantizer triggers dependents before waiting
+  int stream_max_m = 32;       // FLEXQ_STREAM_MAX_M: largest M on the streaming GEMV
+  int stream_stages = -1;      // FLEXQ_STREAM_STAGES: 2/3/4 forced ring depth (-1: by size)
+  int min_units = 4;           // FLEXQ_MIN_UNITS: units per warp with 4-stage rings
+};
+const Tuning& tuning();
+int device_sms();  // SM count of the current device (cached per device)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, bytes)
+cudaError_t ensure_smem(const void* kern, int bytes);
+
 // ---- geometry ------------------------------------------------------------------
 constexpr int kChunkK = 128;   // packing.py:27 MMA_K, one FLXQ-P k-chunk
 constexpr int kKStep = 32;     // mma.m16n8k32 contraction per instruction

@@ -301,26 +301,14 @@ int gemv_stream_launch(const uint32_t*, const void*, int, const uint32_t*, const
                        int, void*, const void*, cudaStream_t);
 
 int64_t tc_act_m_pad(int64_t m);
-bool gemv_dyn_supported(int64_t m, int64_t spg);
-int64_t gemv_dyn_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
-int gemv_dyn_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
-                    const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*,
-                    int, void*, const void*, cudaStream_t);
 bool gemm_tc_supported(int64_t m, int64_t m_pad, int64_t spg);
 int64_t gemm_tc_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
 int gemm_tc_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
                    const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*, int,
                    void*, const void*, cudaStream_t);
 
-// FLEXQ_DISABLE_TC=1 routes M > 16 to the mma.sync kernel (A/B runs)
-static bool tc_enabled() {
-  static int en = -1;
-  if (en < 0) {
-    const char* e = getenv("FLEXQ_DISABLE_TC");
-    en = (e && atoi(e) == 1) ? 0 : 1;
-  }
-  return en == 1;
-}
+// FLEXQ_DISABLE_TC=1 routes M > 16 to the mma.sync kernel (A/B runs; read once, tuning())
+static bool tc_enabled() { return !tuning().disable_tc; }
 
 int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int ksplit) {
   T6Geom G(n, k, gs);
@@ -330,10 +318,6 @@ int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int kspli
       (ksplit <= 0 && (ksplit == 0 || m <= 16) && gemv_stream_supported(m, G.spg, G.rg * G.kb))) {
     const int64_t b2 = gemv_stream_workspace(m, n, k, gs);
     if (b2 > bytes) bytes = b2;
-  }
-  if (ksplit == 0 && gemv_dyn_supported(m, G.spg)) {
-    const int64_t b4 = gemv_dyn_workspace(m, n, k, gs);
-    if (b4 > bytes) bytes = b4;
   }
   if ((ksplit == 0 || ksplit == -2) && gemm_tc_supported(m, tc_act_m_pad(m), G.spg)) {
     const int64_t b3 = gemm_tc_workspace(m, n, k, gs);
@@ -386,10 +370,6 @@ int gemm_t6_launch(const uint32_t* t6, const void* wscale, int scale_f16,
     return gemv_stream_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
                               gs, partials, y, out_dtype, workspace, residual, st);
   }
-  // decode regime, one group per k-block: dynamically scheduled pieces (gemv_dyn.cu)
-  if (ksplit == 0 && gemv_dyn_supported(m, G.spg) && workspace)
-    return gemv_dyn_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,
-                           gs, partials, y, out_dtype, workspace, residual, st);
   // decode regime: the persistent TMA-fed streaming kernel (gemv_stream.cu)
   if (ksplit <= 0 && (ksplit == 0 || m <= 16) && gemv_stream_supported(m, G.spg, G.rg * G.kb) && (workspace || !fast))
     return gemv_stream_launch(t6, wscale, scale_f16, act_frag, act_scale, act_corr, m, m_pad, n, k,

@@ -35,10 +35,6 @@
 // by the last contributor (atomic counter) -- deterministic, as in gemv_stream.cu.
 #include <type_traits>
 
-#ifndef FLEXQ_EXP
-#define FLEXQ_EXP 0  // experiment bits for A/B profiling builds only (results invalid if set)
-#endif
-
 #ifndef FLEXQ_TC_REGACC_MAX
 #define FLEXQ_TC_REGACC_MAX 64  // token tiles up to this width keep the fp32 accumulator in registers
 #endif
@@ -200,7 +196,6 @@ struct TcParams {
   unsigned* counters;
   const void* res;       // optional residual added at the store (same dtype/shape as y)
   long long* trace_clk;  // debug timeline of CTA 0 (FLEXQ_TC_TIMELINE), normally NULL
-  int dbg;               // debug experiment bits (FLEXQ_TC_DBG), results invalid when set
 };
 
 // timeline record: [role][unit][event] clock64 stamps for CTA 0
@@ -904,15 +899,7 @@ bool gemm_tc_supported(int64_t m, int64_t m_pad, int64_t spg) {
   return m_pad >= cdiv(m, tn) * tn;
 }
 
-static int tc_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+static int tc_sms() { return device_sms(); }
 
 static int64_t tc_ctas(int64_t units) { return units < tc_sms() ? units : tc_sms(); }
 
@@ -928,11 +915,9 @@ template <int TN, bool SF16, bool TRACE, bool FAST, int OUT>
 static int launch_tc_inst(const TcParams& p, cudaStream_t st) {
   auto kern = gemm_tc_kernel<TN, SF16, TRACE, FAST, OUT>;
   constexpr int smem = TcCfg<TN>::kBytes;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {  // once per (device, instantiation)
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return cuda_status(e, "gemm_tc attribute");
-    configured = true;
   }
   cudaError_t e = launch_pdl(kern, dim3((unsigned)p.nctas), dim3(TcCfg<TN>::kThreads), (size_t)smem, st, p);
   if (e != cudaSuccess) return cuda_status(e, "gemm_tc launch");
@@ -1004,8 +989,7 @@ int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const 
   p.partials = partials;
   p.y = y;
   p.res = residual;
-  if (getenv("FLEXQ_TC_DBG")) p.dbg = atoi(getenv("FLEXQ_TC_DBG"));
-  if (getenv("FLEXQ_TC_TIMELINE")) {
+  if (tuning().tc_timeline) {
     if (!g_tl) cudaMalloc(&g_tl, (kTlRoles * kTlUnits * 4 + 4 * 1024) * sizeof(long long));
     cudaMemsetAsync(g_tl, 0, (kTlRoles * kTlUnits * 4 + 4 * 1024) * sizeof(long long), st);
     p.trace_clk = g_tl;

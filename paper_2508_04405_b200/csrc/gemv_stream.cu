@@ -566,14 +566,7 @@ extern "C" int flexq_debug_gemv_timeline(long long* host, int max_entries) {
 
 // M <= 16 for every group layout; 16 < M <= 32 (MT = 4) for one group per k-block, where the
 // mma.sync stream beats the tcgen05 kernel (FLEXQ_STREAM_MAX_M = 16 turns it off)
-static int64_t stream_max_m() {
-  static int64_t v = 0;
-  if (!v) {
-    const char* e = getenv("FLEXQ_STREAM_MAX_M");
-    v = (e && atoi(e) >= 1) ? atoi(e) : 32;
-  }
-  return v;
-}
+static int64_t stream_max_m() { return tuning().stream_max_m; }
 // M in (16, 32] only for layers of >= 8192 units (48 MB of T6 weights): smaller layers have
 // too few units per warp to hide the MT = 4 split fixup, and tcgen05 is faster there
 // (LLaMA-2-7B shapes, tools/sweep.py r01)
@@ -583,15 +576,7 @@ bool gemv_stream_supported(int64_t m, int64_t spg, int64_t units) {
   return m <= 32 && stream_mode(spg) == 0 && units >= 8192;
 }
 
-static int stream_stages() {
-  static int s = 0;
-  if (!s) {
-    const char* e = getenv("FLEXQ_STREAM_STAGES");  // tuning knob for A/B runs (2/3/4)
-    const int v = e ? atoi(e) : 0;
-    s = (v >= 2 && v <= 4) ? v : -1;  // -1: automatic
-  }
-  return s;
-}
+static int stream_stages() { return tuning().stream_stages; }  // -1: automatic (A/B knob)
 
 template <int MT, int MODE, bool SF16, bool TRACE, bool FAST, int OUT, int S>
 static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
@@ -599,14 +584,11 @@ static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
                                     : gemv_t6_stream_kernel<MT, MODE, SF16, TRACE, FAST, OUT, S, false>;
   constexpr int UB = StageLayout<MT, MODE, SF16>::kBytes;
   constexpr int kMaxW = max_warps<MT>();
-  static const bool wide = getenv("FLEXQ_GEMV_WIDE") != nullptr;
-  static bool configured[2] = {false, false};  // one attribute call per instantiation
-  const int ci = (MT == 1 && p.m == 1) ? 1 : 0;
-  if (!configured[ci]) {
+  const bool wide = tuning().gemv_wide;
+  {  // once per (device, instantiation)
     const int cap = kMaxW * S * (UB + 8) < 227 * 1024 ? kMaxW * S * (UB + 8) : 227 * 1024;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), cap);
     if (e != cudaSuccess) return cuda_status(e, "gemv_stream attribute");
-    configured[ci] = true;
   }
   int wpc = kSWarps, per_sm = 0;  // warps per CTA, CTAs per SM
   if (wide) {  // one CTA per SM with as many warps as the SM's shared memory holds
@@ -623,11 +605,7 @@ static int launch_stream_inst(StreamParams p, int num_sms, cudaStream_t st) {
   int64_t warps = (int64_t)num_sms * per_sm * wpc;
   // bounds the fixup fan-in; deep rings (small layers) spread the units thinner so that a
   // warp's whole range is in flight at once
-  static int min_deep = 0;  // units per warp with 4-stage rings (tuning knob FLEXQ_MIN_UNITS)
-  if (!min_deep) {
-    const char* e = getenv("FLEXQ_MIN_UNITS");
-    min_deep = (e && atoi(e) > 0) ? atoi(e) : 4;
-  }
+  const int min_deep = tuning().min_units;  // units per warp with 4-stage rings
   const int64_t by_units = cdiv(p.units, S >= 4 ? min_deep : kMinUnitsPerWarp);
   if (warps > by_units) warps = by_units;
   p.nw = warps;
@@ -680,12 +658,7 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
     set_error("gemv_stream: workspace required");
     return FLEXQ_ERR_CONFIG;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = device_sms();
   StreamParams p{};
   p.t6 = reinterpret_cast<const uint8_t*>(t6);
   p.wscale = wscale;
@@ -699,10 +672,10 @@ int gemv_stream_launch(const uint32_t* t6, const void* wscale, int scale_f16,
   p.partials = partials;
   p.y = y;
   p.res = residual;
-  if (getenv("FLEXQ_GEMV_REV")) p.rev = 1;
+  if (tuning().gemv_rev) p.rev = 1;
   p.dbg = dbg_trace_buf();
   if (p.dbg) p.dbg_tag = dbg_next_launch() << 8 | 2;
-  if (getenv("FLEXQ_GEMV_TIMELINE")) {
+  if (tuning().gemv_timeline) {
     static long long* tlbuf = nullptr;
     if (!tlbuf) cudaMalloc(&tlbuf, 148 * 16 * 8 * sizeof(long long));
     cudaMemsetAsync(tlbuf, 0, 148 * 16 * 8 * sizeof(long long), st);

@@ -338,12 +338,7 @@ static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
   const int64_t items = A.rows * A.ng;
   if (DT == FLEXQ_DT_F16 && A.gs == 128 && A.cols % 128 == 0 &&
       reinterpret_cast<uintptr_t>(A.x) % 8 == 0) {
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms();
     // decode batches feed the persistent GEMV (3 CTAs per SM, registers nearly full): at most
     // one quantizer CTA per SM.  Larger batches keep one warp per item (one wave).
     const int64_t ctas = (A.rows <= 16 && cdiv(items, 8) > sms) ? sms : cdiv(items, 8);
@@ -391,8 +386,7 @@ int quantize_launch(const void* x, int dtype, int64_t rows, int64_t cols, int bi
               reinterpret_cast<uint8_t*>(act_frag), act_scale, act_corr, m_pad, flag,
               geo.spg, geo.kb};
   A.dbg = dbg_trace_buf();
-  static const int q_early = getenv("FLEXQ_Q_EARLY") ? 1 : 0;
-  A.early = q_early;
+  A.early = tuning().q_early ? 1 : 0;
   if (A.dbg) A.dbg_tag = dbg_next_launch() << 8 | 1;
   switch (dtype) {
     case FLEXQ_DT_F16: launch_quantize<FLEXQ_DT_F16>(A, st); break;

@@ -1,3 +1,7 @@
+// EXPERIMENT (not built into libflexq_sm100a.so; round 1, opt-in FLEXQ_GEMV_DYN=1 until round 2):
+// dynamically scheduled GEMV pieces.  Removed the per-warp spread but its claim / fixup
+// atomics cost more than they saved (70B gate M=1: 34.1 -> 42.6 us), DESIGN.md sec. 4.1.
+// Kept for the record; it compiled against the round-1 gemm_t6.cu dispatch.
 // Decode-regime T6 GEMV with dynamic piece scheduling (group = one k-block, e.g. g = 128).
 //
 // Same math, stage layout and TMA ring as gemv_stream.cu, but the work is cut into fixed
