@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=2.0,
                     help="seconds of CPU work per sampled cpu_baseline step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--bitserial", action="store_true",
-                    help="also time the BTC-equivalent bit-serial kernel (extra key)")
+    ap.add_argument("--no-bitserial", action="store_true",
+                    help="skip timing the BTC-equivalent AND+popcount kernel (the north star's "
+                         "bit-serial vs unpack-to-INT8 decision, extra key 'bitserial')")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the M=8 and config-1 companion measurements")
     return ap.parse_args()
@@ -426,7 +427,7 @@ def main():
     }
     if world == 1 and not args.no_extra:
         line["extra"] = extra_lines(torch, dist, FlexQLinear, layers, shapes, args, dev)
-    if args.bitserial and world == 1:
+    if not args.no_bitserial and world == 1:
         line["bitserial"] = time_bitserial(layers, M, shapes)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Impl, calibrate_rows, kind = cpu_baseline_impl()
