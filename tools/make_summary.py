@@ -57,6 +57,8 @@ def main(tag):
                 "|---|---|---|---|---|---|---|---|---|---|---|"]
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         from sweep import kernel_name
+        comp = {(r["layer"], r["m"]): r for r in rows if r.get("comparator")}
+        rows = [r for r in rows if not r.get("comparator")]
         for r in rows:
             r["kernel"] = kernel_name(r["m"], r["n"], r["k"])
             out.append(f"| {r['layer']} | {r['n']}x{r['k']} | {r['m']} | {r['kernel']} | "
@@ -64,6 +66,18 @@ def main(tag):
                        f"{r['frac_hbm']:.2f} | {r['tops_gemm']:.1f} | "
                        f"{r.get('us_tc', float('nan')):.1f} | "
                        f"{r.get('us_mma_sync', float('nan')):.1f} |")
+        if comp:
+            out += ["", f"cuBLAS comparators, {mdl} (same layers, weights rotated over > 2x L2; "
+                        "W16A16 `torch.matmul`, W8A8 `torch._int_mm` int32 out -- no dequant, "
+                        "M > 16 only):", "",
+                    "| layer | M | this repo GEMM us | this repo fwd us | cuBLAS fp16 us | cuBLASLt int8 us |",
+                    "|---|---|---|---|---|---|"]
+            for r in rows:
+                c = comp.get((r["layer"], r["m"]))
+                if c:
+                    i8 = c.get("us_cublas_i8")
+                    out.append(f"| {r['layer']} | {r['m']} | {r['us_gemm']:.1f} | {r['us_fwd']:.1f} | "
+                               f"{c['us_cublas_f16']:.1f} | {'-' if i8 is None else f'{i8:.1f}'} |")
     # decode
     p = os.path.join(src, f"{tag}_decode_7b.jsonl")
     rows = load_jsonl(p)
