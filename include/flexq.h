@@ -166,6 +166,26 @@ int flexq_group_epilogue_f64(const int32_t* partials, const double* wscale,
                              const double* xscale, int64_t m, int64_t n, int64_t groups,
                              double* y, uint16_t* y16, cudaStream_t stream);
 
+/* ---- batched fast path with the scales folded into fp16 operands ---------
+ * For 32 < M <= 128 at group 128 with fp16 weight scales, flexq_linear_forward(_ex) runs
+ * tcgen05.mma.kind::f16 over A = fp16(w * ws) (converted on chip from the T6 stream) and
+ * B = fp16(x_code * xs) (written by the activation quantizer), accumulating each tile's whole
+ * K range in fp32 TMEM (csrc/gemm_tc16.cu).  Same codes and scales as the
+ * reference (quantize.py:118-148); fp16 y within the fast path's tolerance; no INT32 partials
+ * (flexq_gemm_t6 with `partials` gives those).  act_f16: the fp16 operand inside an act buffer
+ * (flexq_act_f16_operand); workspace: flexq_gemm_workspace_bytes(m, n, k, 128, 0). */
+#define FLEXQ_KERNEL_GEMV 0      /* streaming GEMV (mma.sync), decode batches */
+#define FLEXQ_KERNEL_TC_I8 1     /* tcgen05 kind::i8, exact INT32 group partials */
+#define FLEXQ_KERNEL_TC16 2      /* tcgen05 kind::f16, scales folded into the operands */
+#define FLEXQ_KERNEL_MMA_SYNC 3  /* mma.sync (group sizes not aligned to 128 k) */
+/* The GEMM kernel flexq_linear_forward uses for this shape (the FLEXQ_KERNEL_* codes). */
+int flexq_linear_kernel(int64_t m, int64_t n, int64_t k, int64_t group_size, int scale_f16);
+int flexq_gemm_tc16(const uint32_t* t6, const void* wscale, const void* act_f16, int64_t m,
+                    int64_t n, int64_t k, void* y, int out_dtype, void* workspace,
+                    const void* residual, cudaStream_t stream);
+/* Address of the fp16 operand inside an act buffer of flexq_act_buf_bytes(m, k, group_size). */
+void* flexq_act_f16_operand(void* act_buf, int64_t m, int64_t k, int64_t group_size);
+
 /* ---- one-call online linear (quantized_linear with pre-packed weights) ----
  * Replaces the online half of quantized_linear (engine.py:487-513):
  * quantize activations (fp16 [m, k]) -> T6 GEMM -> fp16 y [m, n].

@@ -18,6 +18,7 @@ OK, ERR_INVALID, ERR_SHAPE, ERR_CONFIG, ERR_FORMAT, ERR_CUDA = 0, -1, -2, -3, -4
 FLAG_NONFINITE, FLAG_NONPOS_SCALE, FLAG_KV_OVERFLOW = 1, 2, 4
 DT_F16, DT_BF16, DT_F32, DT_F64 = 0, 1, 2, 3
 OUT_F16, OUT_F32 = 0, 1
+KERNEL_GEMV, KERNEL_TC_I8, KERNEL_TC16, KERNEL_MMA_SYNC = 0, 1, 2, 3
 
 _EXC = {ERR_INVALID: InvalidInputError, ERR_SHAPE: ShapeError, ERR_CONFIG: ConfigError,
         ERR_FORMAT: FormatError, ERR_CUDA: DeviceError}
@@ -50,6 +51,9 @@ SIGNATURES = {
     "flexq_linear_forward": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, vp, vp, vp, vp]),
     "flexq_linear_forward_ex": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, i32, vp, vp, vp,
                                       vp, vp]),
+    "flexq_linear_kernel": (i32, [i64, i64, i64, i64, i32]),
+    "flexq_gemm_tc16": (i32, [vp, vp, vp, i64, i64, i64, vp, i32, vp, vp, vp]),
+    "flexq_act_f16_operand": (vp, [vp, i64, i64, i64]),
     "flexq_rmsnorm_quantize": (i32, [vp, i64, vp, ctypes.c_float, i64, i64, i32, i64, vp, vp, vp,
                                      i64, vp, vp, vp]),
     "flexq_silu_mul_quantize": (i32, [vp, i64, i64, i64, i32, i64, vp, vp, vp, i64, vp, vp, vp]),

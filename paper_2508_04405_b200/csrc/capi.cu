@@ -55,6 +55,12 @@ int attn_decode_launch(const void*, const void*, const void*, const int*, void*,
 int attn_block_launch(const void*, const int*, void*, void*, void*, int64_t, int, int, int64_t,
                       float, int, int64_t, uint32_t*, float*, int32_t*, int64_t, uint32_t*,
                       cudaStream_t);
+bool gemm_tc16_supported(int64_t, int64_t, int64_t, int64_t, int);
+int gemm_tc16_launch(const uint32_t*, const void*, const void*, int64_t, int64_t, int64_t, void*,
+                     int, void*, const void*, cudaStream_t);
+int quantize_f16op_launch(const void*, int64_t, int64_t, int, __half*, int64_t, uint32_t*,
+                          cudaStream_t);
+bool gemv_stream_supported(int64_t m, int64_t spg, int64_t units);
 int group_epilogue_launch(const int32_t*, const double*, const double*, int64_t, int64_t, int64_t,
                           double*, uint16_t*, cudaStream_t);
 
@@ -79,6 +85,7 @@ const Tuning& tuning() {
     v.gemv_timeline = env("FLEXQ_GEMV_TIMELINE") != nullptr;
     v.tc_timeline = env("FLEXQ_TC_TIMELINE") != nullptr;
     v.q_early = env("FLEXQ_Q_EARLY") != nullptr;
+    v.disable_tc16 = env("FLEXQ_DISABLE_TC16") && atoi(env("FLEXQ_DISABLE_TC16")) == 1;
     if (env("FLEXQ_STREAM_MAX_M") && atoi(env("FLEXQ_STREAM_MAX_M")) >= 1)
       v.stream_max_m = atoi(env("FLEXQ_STREAM_MAX_M"));
     if (env("FLEXQ_STREAM_STAGES")) {
@@ -173,6 +180,7 @@ const char* flexq_tuning(void) {
     if (t.gemv_timeline != d.gemv_timeline) add("FLEXQ_GEMV_TIMELINE", "1");
     if (t.tc_timeline != d.tc_timeline) add("FLEXQ_TC_TIMELINE", "1");
     if (t.q_early != d.q_early) add("FLEXQ_Q_EARLY", "1");
+    if (t.disable_tc16 != d.disable_tc16) add("FLEXQ_DISABLE_TC16", "1");
     if (t.stream_max_m != d.stream_max_m) add("FLEXQ_STREAM_MAX_M", std::to_string(t.stream_max_m));
     if (t.stream_stages != d.stream_stages) add("FLEXQ_STREAM_STAGES", std::to_string(t.stream_stages));
     if (t.min_units != d.min_units) add("FLEXQ_MIN_UNITS", std::to_string(t.min_units));
@@ -317,12 +325,46 @@ int flexq_group_epilogue_f64(const int32_t* partials, const double* wscale,
 
 int64_t flexq_act_m_pad(int64_t m) { return m < 1 ? 0 : tc_act_m_pad(m); }
 
-int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size) {
+// The batched forward takes the kind::f16 kernel (gemm_tc16.cu) for 32 < m <= 128 at group 128
+// with fp16 weight scales; the fp16 operand then follows the INT8 operand in the act buffer.
+static bool tc16_route(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f16) {
+  return m > 32 && !tuning().disable_tc16 && !tuning().disable_tc &&
+         gemm_tc16_supported(m, n, k, gs, scale_f16);
+}
+
+static int64_t act_f16_offset(int64_t m, int64_t k, int64_t group_size) {
   const int64_t m_pad = flexq_act_m_pad(m);
   T6Geom G(1, k, group_size);
   const int64_t frag = cdiv(flexq_act_frag_bytes(m_pad, k, group_size), 256) * 256;
   const int64_t vec = cdiv(G.ng * m_pad * 4, 256) * 256;
   return frag + 2 * vec;
+}
+
+int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size) {
+  const int64_t base = act_f16_offset(m, k, group_size);
+  if (m > 32 && group_size == 128 && k % 128 == 0)  // room for the fp16 operand (gemm_tc16)
+    return base + flexq_act_m_pad(m) * k * 2;
+  return base;
+}
+
+int flexq_linear_kernel(int64_t m, int64_t n, int64_t k, int64_t group_size, int scale_f16) {
+  if (m < 1 || n < 1 || k < 1 || group_size < 1) return -1;
+  if (tc16_route(m, n, k, group_size, scale_f16)) return FLEXQ_KERNEL_TC16;
+  T6Geom G(n, k, group_size);
+  if (gemv_stream_supported(m, G.spg, G.rg * G.kb)) return FLEXQ_KERNEL_GEMV;
+  if (m > 16 && G.spg % 4 == 0 && !tuning().disable_tc) return FLEXQ_KERNEL_TC_I8;
+  return FLEXQ_KERNEL_MMA_SYNC;
+}
+
+int flexq_gemm_tc16(const uint32_t* t6, const void* wscale, const void* act_f16, int64_t m,
+                    int64_t n, int64_t k, void* y, int out_dtype, void* workspace,
+                    const void* residual, cudaStream_t stream) {
+  return gemm_tc16_launch(t6, wscale, act_f16, m, n, k, y, out_dtype, workspace, residual, stream);
+}
+
+void* flexq_act_f16_operand(void* act_buf, int64_t m, int64_t k, int64_t group_size) {
+  if (!act_buf) return nullptr;
+  return reinterpret_cast<char*>(act_buf) + act_f16_offset(m, k, group_size);
 }
 
 static int linear_forward(const uint32_t* t6, const void* wscale, int scale_f16, int xbits,
@@ -345,6 +387,12 @@ static int linear_forward(const uint32_t* t6, const void* wscale, int scale_f16,
   uint32_t* act_frag = reinterpret_cast<uint32_t*>(base);
   float* xs = reinterpret_cast<float*>(base + frag);
   int32_t* corr = reinterpret_cast<int32_t*>(base + frag + vec);
+  if (tc16_route(m, n, k, group_size, scale_f16)) {  // batched: scales folded into fp16 operands
+    __half* act16 = reinterpret_cast<__half*>(base + frag + 2 * vec);
+    int rc = quantize_f16op_launch(x, m, k, xbits, act16, m_pad, flag, stream);
+    if (rc) return rc;
+    return gemm_tc16_launch(t6, wscale, act16, m, n, k, y, out_dtype, workspace, residual, stream);
+  }
   int rc = quantize_launch(x, FLEXQ_DT_F16, m, k, xbits, group_size, 1, nullptr, nullptr,
                            act_frag, xs, corr, m_pad, flag, stream);
   if (rc) return rc;

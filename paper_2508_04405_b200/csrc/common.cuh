@@ -32,6 +32,7 @@ struct Tuning {
   bool gemv_timeline = false;  // FLEXQ_GEMV_TIMELINE: per-warp GEMV timeline
   bool tc_timeline = false;    // FLEXQ_TC_TIMELINE: tcgen05 CTA-0 timeline
   bool q_early = false;        // FLEXQ_Q_EARLY: quantizer triggers dependents before waiting
+  bool disable_tc16 = false;   // FLEXQ_DISABLE_TC16=1: batched forwards on the INT8 tcgen05 kernel
   int stream_max_m = 32;       // FLEXQ_STREAM_MAX_M: largest M on the streaming GEMV
   int stream_stages = -1;      // FLEXQ_STREAM_STAGES: 2/3/4 forced ring depth (-1: by size)
   int min_units = 4;           // FLEXQ_MIN_UNITS: units per warp with 4-stage rings

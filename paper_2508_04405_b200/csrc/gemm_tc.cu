@@ -210,9 +210,14 @@ __device__ __forceinline__ long long gtimer() {
 __device__ __forceinline__ void cta_mark(const TcParams& p, int ev, long long v) {
   if (p.trace_clk) p.trace_clk[kTlRoles * kTlUnits * 4 + blockIdx.x * 4 + ev] = v;
 }
+#ifndef FLEXQ_TC_TIMELINE_MARKS
+#define FLEXQ_TC_TIMELINE_MARKS 0  // debug builds only (the marks cost ~30 % of the loop, measured)
+#endif
 __device__ __forceinline__ void tl_mark(const TcParams& p, int role, int64_t i, int ev) {
-  if (p.trace_clk && blockIdx.x == 0 && i < kTlUnits)
-    p.trace_clk[(role * kTlUnits + i) * 4 + ev] = clock64();
+  if constexpr (FLEXQ_TC_TIMELINE_MARKS) {
+    if (p.trace_clk && blockIdx.x == 0 && i < kTlUnits)
+      p.trace_clk[(role * kTlUnits + i) * 4 + ev] = clock64();
+  }
 }
 
 __device__ __forceinline__ int64_t tc_unit_start(int64_t c, int64_t units, int64_t P) {

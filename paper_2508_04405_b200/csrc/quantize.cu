@@ -51,6 +51,10 @@ struct QuantArgs {
   long long* dbg = nullptr;  // FLEXQ_TRACE event buffer (debug)
   long long dbg_tag = 0;
   int early = 0;  // experiment (FLEXQ_Q_EARLY): trigger dependents before waiting
+  // optional fp16 operand of the kind::f16 batched kernel (gemm_tc16.cu): fp16(code * scale)
+  // at [k-block][m_pad/8][16 cores][8 tokens][16 B], position p = 16(2t+h) + 4jj + b of slot
+  // 32jj + 16h + 4t + b (the same permutation as act_frag); group 128 fast path only
+  __half* act_f16 = nullptr;
 };
 
 // Byte of (token m, logical column c) in the activation operand:
@@ -307,6 +311,18 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
     if (A.codes) *reinterpret_cast<uint32_t*>(A.codes + r * A.cols + g * 128 + lane * 4) = word;
     if (A.act_frag)
       *reinterpret_cast<uint32_t*>(A.act_frag + operand_word_offset(g, r, A.m_pad, lane)) = word;
+    if (A.act_f16) {  // fp16(code * scale): the product is exact in double, one rounding
+      __half hv[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int code = (int)(int8_t)((word >> (8 * i)) & 0xffu);
+        hv[i] = __double2half((double)code * sc);
+      }
+      // columns 4L .. 4L+3 of the group: core L / 2 (8 k each), bytes 8 (L % 2) ..
+      uint8_t* dst = reinterpret_cast<uint8_t*>(A.act_f16) +
+                     ((g * (A.m_pad >> 3) + (r >> 3)) * 16 + (lane >> 1)) * 128 + (r & 7) * 16 + 8 * (lane & 1);
+      *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(hv);
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
     if (lane == 0) {
@@ -352,6 +368,25 @@ static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
   } else {
     launch_pdl(quantize_cta_kernel<DT>, dim3((unsigned)items), dim3(1024), 0, st, A);
   }
+}
+
+// fp16 input, group 128, K % 128 == 0: codes -> the fp16 operand of gemm_tc16 only
+int quantize_f16op_launch(const void* x, int64_t rows, int64_t cols, int bits, __half* act_f16,
+                          int64_t m_pad, uint32_t* flag, cudaStream_t st) {
+  if (rows < 1 || cols % 128 || bits < 2 || bits > 8 || !flag || !act_f16 || m_pad < rows ||
+      m_pad % kTokTile || reinterpret_cast<uintptr_t>(x) % 8) {
+    set_error("quantize_f16op: bad arguments (rows=%lld cols=%lld bits=%d)", (long long)rows,
+              (long long)cols, bits);
+    return FLEXQ_ERR_INVALID_INPUT;
+  }
+  T6Geom geo(m_pad, cols, 128);
+  QuantArgs A{x, rows, cols, 128, geo.ng, bits, 1, nullptr, nullptr, nullptr, nullptr, nullptr,
+              m_pad, flag, geo.spg, geo.kb};
+  A.act_f16 = act_f16;
+  A.early = tuning().q_early ? 1 : 0;
+  launch_quantize<FLEXQ_DT_F16>(A, st);
+  FLEXQ_LAUNCH_CHECK("quantize_f16op");
+  return FLEXQ_OK;
 }
 
 int quantize_launch(const void* x, int dtype, int64_t rows, int64_t cols, int bits, int64_t gs,

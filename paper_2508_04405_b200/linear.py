@@ -56,6 +56,7 @@ class FlexQLinear:
                                                scale_f16=self.fp16_scales)
         self.device = codes.device
         self._bufs: dict[int, tuple] = {}
+        self._f16_ready: set[int] = set()  # batches whose act buffer holds the fp16 operand
         self.flag = t.zeros(1, dtype=t.int32, device=self.device)
 
     # -- construction from reference artefacts ------------------
@@ -192,6 +193,9 @@ class FlexQLinear:
         if residual is not None:
             self._check_out("residual", residual, m, out_dtype)
         act, ws = self.buffers(m)
+        if _lib.lib().flexq_linear_kernel(m, self.n, self.k, self.group_size,
+                                          int(self.fp16_scales)) == _lib.KERNEL_TC16:
+            self._f16_ready.add(m)
         _lib.check(_lib.lib().flexq_linear_forward_ex(
             _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), self.activation_bits,
             _lib.ptr(x), m, self.n, self.k, self.group_size, _lib.ptr(out),
@@ -220,8 +224,19 @@ class FlexQLinear:
         self._check_out("out", out, m, out.dtype if out.dtype in (t.float16, t.float32) else t.float16)
         if residual is not None:
             self._check_out("residual", residual, m, out.dtype)
+        L = _lib.lib()
+        act, ws = self.buffers(m)
+        if m in self._f16_ready:
+            # batched route: the fp16 operand the last forward(m) wrote (scales folded in);
+            # operands written by other producers (the decode harness's fused quantizers) are
+            # the INT8 layout and take the integer kernels below
+            op = L.flexq_act_f16_operand(act.data_ptr(), m, self.k, self.group_size)
+            _lib.check(L.flexq_gemm_tc16(
+                _lib.ptr(self.t6), _lib.ptr(self.wscale), op, m, self.n, self.k, _lib.ptr(out),
+                _lib.OUT_F32 if out.dtype == t.float32 else _lib.OUT_F16, _lib.ptr(ws),
+                _lib.ptr(residual), _lib.stream()))
+            return out
         frag, xs, corr, m_pad = self._act_views(m)
-        _, ws = self.buffers(m)
         _lib.check(_lib.lib().flexq_gemm_t6_ex(
             _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), frag, xs, corr, m,
             m_pad, self.n, self.k, self.group_size, None, _lib.ptr(out),

@@ -188,3 +188,34 @@ def test_fused_residual_epilogue(m):
     y2 = torch.empty_like(r)
     lin.forward(x, out=y2, residual=r)  # separate residual buffer
     assert torch.equal(y2, y)
+
+
+@pytest.mark.parametrize("m,n,k,q", [
+    (33, 256, 1024, 6),       # smallest tile-64 batch
+    (48, 136, 2048, 8),       # odd row count: half-empty last 128-row tile
+    (64, 1000, 4096, 6),      # N not a multiple of 128, split tiles
+    (100, 640, 8192, 8),      # tile 128, deep stream-K
+    (128, 384, 28672, 8),     # down_proj K: 224 k-blocks
+])
+def test_tc16_fast_path(m, n, k, q):
+    """The batched fast path (csrc/gemm_tc16.cu: tcgen05 kind::f16 over fp16(w*ws) and
+    fp16(code*xs), fp32 accumulation): the same quantizer codes and scales as the reference,
+    fp16 y within max|y - y_ref| <= 1e-3 * max|y_ref| of int_matmul_reference (engine.py:
+    337-365); gemm_only replays the identical output; run to run bit-identical."""
+    L = _lib.lib()
+    assert L.flexq_linear_kernel(m, n, k, 128, 1) == _lib.KERNEL_TC16
+    w, x, _, y_ref, _ = case(m, n, k, q, 128, seed=17 * m + n)
+    lin = fq.FlexQLinear(w, activation_bits=q)
+    xd = torch.from_numpy(x).cuda()
+    y = lin(xd)
+    assert max_rel(y.float().cpu().numpy(), y_ref) <= FP16_TOL
+    y2 = lin(xd)
+    assert torch.equal(y, y2)
+    y3 = torch.empty_like(y)
+    lin.gemm_only(m, y3)
+    assert torch.equal(y, y3)
+    r = torch.randn_like(y)
+    y4 = r.clone()
+    lin.forward(xd, out=y4, residual=y4)
+    assert torch.allclose(y4.float(), y.float() + r.float(), atol=1e-2, rtol=2e-3)
+    lin.check_errors()

@@ -84,6 +84,7 @@ def main():
             c = object.__new__(FlexQLinear)
             c.__dict__.update(base.__dict__)
             c.t6, c.wscale, c._bufs = base.t6.clone(), base.wscale.clone(), {}
+            c._f16_ready = set()
             c.flag = torch.zeros(1, dtype=torch.int32, device=dev)
             lays.append(c)
         for m in ms:
