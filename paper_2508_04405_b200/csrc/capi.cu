@@ -328,8 +328,12 @@ int64_t flexq_act_m_pad(int64_t m) { return m < 1 ? 0 : tc_act_m_pad(m); }
 // The batched forward takes the kind::f16 kernel (gemm_tc16.cu) for 32 < m <= 128 at group 128
 // with fp16 weight scales; the fp16 operand then follows the INT8 operand in the act buffer.
 static bool tc16_route(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f16) {
-  return m > 32 && !tuning().disable_tc16 && !tuning().disable_tc &&
-         gemm_tc16_supported(m, n, k, gs, scale_f16);
+  if (m <= 32 || tuning().disable_tc16 || tuning().disable_tc || !gemm_tc16_supported(m, n, k, gs, scale_f16))
+    return false;
+  // 128 < M <= 256 (one 256-token tile, a single TMEM accumulator): faster than the INT8
+  // kernel on layers of >= 8192 units (70B gate 122 vs 186 us), not on smaller ones
+  // (70B qkv 82 vs 79 us; tools/ab_tc16.sh)
+  return m <= 128 || cdiv(n, 64) * cdiv(k, 128) >= 8192;
 }
 
 static int64_t act_f16_offset(int64_t m, int64_t k, int64_t group_size) {

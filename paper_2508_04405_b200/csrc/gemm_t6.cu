@@ -302,6 +302,7 @@ int gemv_stream_launch(const uint32_t*, const void*, int, const uint32_t*, const
 
 int64_t tc_act_m_pad(int64_t m);
 bool gemm_tc_supported(int64_t m, int64_t m_pad, int64_t spg);
+int64_t gemm_tc16_workspace(int64_t m, int64_t n);
 int64_t gemm_tc_workspace(int64_t m, int64_t n, int64_t k, int64_t gs);
 int gemm_tc_launch(const uint32_t*, const void*, int, const uint32_t*, const float*,
                    const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, int32_t*, void*, int,
@@ -322,6 +323,10 @@ int64_t gemm_t6_workspace(int64_t m, int64_t n, int64_t k, int64_t gs, int kspli
   if ((ksplit == 0 || ksplit == -2) && gemm_tc_supported(m, tc_act_m_pad(m), G.spg)) {
     const int64_t b3 = gemm_tc_workspace(m, n, k, gs);
     if (b3 > bytes) bytes = b3;
+  }
+  if (ksplit == 0 && m > 32 && m <= 256 && gs == 128) {  // the kind::f16 batched forward
+    const int64_t b6 = gemm_tc16_workspace(m, n);
+    if (b6 > bytes) bytes = b6;
   }
   return bytes;
 }

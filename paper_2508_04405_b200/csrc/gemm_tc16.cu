@@ -1,4 +1,4 @@
-// Batched (32 < M <= 128) W6Ax fast path on tcgen05 kind::f16: the group scales are applied to
+// Batched (32 < M <= 256) W6Ax fast path on tcgen05 kind::f16: the group scales are applied to
 // the OPERANDS, so the tensor core accumulates the whole K range of a tile in one fp32 TMEM
 // accumulator and the epilogue runs once per tile instead of once per 128-k group.
 //
@@ -128,8 +128,11 @@ constexpr int kT16WsSlice = kRowGroup * 8 * 4;  // fp16 scale pairs of one row g
 
 template <int TN>
 struct T16Cfg {
-  static constexpr int SW = TN == 128 ? 6 : 8;                   // raw ring (HBM latency)
-  static constexpr int SA = 4;                                   // operand ring (A in TMEM, B in smem)
+  static constexpr int SW = TN >= 128 ? 6 : 8;                   // raw ring (HBM latency)
+  // operand ring (A in TMEM, B in smem); TN = 256 (128 < M <= 256): 64 KB B tiles, so two
+  // stages and a single tile accumulator (256 + 2 x 64 TMEM columns)
+  static constexpr int SA = TN == 256 ? 2 : TN == 128 ? 4 : 6;
+  static constexpr int NACC = TN == 256 ? 1 : 2;                 // tile accumulators in TMEM
   static constexpr int kRaw = 2 * (kUnitBytes + kT16WsSlice);    // two row groups + scales
   static constexpr int kB = TN * 256;                            // TN tokens x 128 fp16
   static constexpr int kOffRaw = 0;
@@ -138,8 +141,8 @@ struct T16Cfg {
   static constexpr int kNumBars = 2 * SW + 2 * SA + 4;
   static constexpr int kBytes = kOffBar + kNumBars * 8 + 16;
   static_assert(kBytes <= 232448, "shared memory budget");
-  static constexpr int kAcolBase = 2 * TN;
-  static_assert(2 * TN + SA * 64 <= 512, "TMEM budget");
+  static constexpr int kAcolBase = NACC * TN;
+  static_assert(NACC * TN + SA * 64 <= 512, "TMEM budget");
   static constexpr uint32_t kTmemCols = 512;
   // D f32 (bits 4-5 = 1), A f16 (7-9 = 0), B f16 (10-12 = 0), K-major; N >> 3, M >> 4
   static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -161,16 +164,27 @@ struct T16Params {
   long long* tl;  // debug timeline of CTA 0 (FLEXQ_TC_TIMELINE): [role][unit][4] clock64
 };
 
-constexpr int kT16TlUnits = 64;
 #ifndef FLEXQ_TC16_TIMELINE
-#define FLEXQ_TC16_TIMELINE 0  // debug builds only: per-role clock64 marks of CTA 0
+#define FLEXQ_TC16_TIMELINE 0  // debug builds only (-DFLEXQ_TC16_TIMELINE=1)
 #endif
-__device__ __forceinline__ void t16_mark(const T16Params& p, int role, int64_t i, int ev) {
-  if constexpr (FLEXQ_TC16_TIMELINE) {
-    if (p.tl && blockIdx.x == 0 && i < kT16TlUnits) p.tl[(role * kT16TlUnits + i) * 4 + ev] = clock64();
+// Debug profile of CTA 0: every role sums the cycles it spends in each phase in registers and
+// writes the totals once at the end (per-event stores in the loops cost up to 30 %).
+struct T16Prof {
+  long long acc[4] = {0, 0, 0, 0};
+  long long t = 0;
+  __device__ void start() { if constexpr (FLEXQ_TC16_TIMELINE) t = clock64(); }
+  __device__ void lap(int i) {
+    if constexpr (FLEXQ_TC16_TIMELINE) { const long long n = clock64(); acc[i] += n - t; t = n; }
   }
-}
-
+  __device__ void flush(const T16Params& p, int role, int64_t units) {
+    if constexpr (FLEXQ_TC16_TIMELINE) {
+      if (p.tl && blockIdx.x == 0) {
+        for (int i = 0; i < 4; i++) p.tl[role * 8 + i] = acc[i];
+        p.tl[role * 8 + 4] = units;
+      }
+    }
+  }
+};
 __device__ __forceinline__ int64_t t16_start(int64_t c, int64_t units, int64_t P) { return c * units / P; }
 __device__ __forceinline__ int64_t t16_owner(int64_t u, int64_t units, int64_t P) { return ((u + 1) * P - 1) / units; }
 
@@ -219,9 +233,13 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
     const uint32_t tlane = tmem + ((uint32_t)(16 * r8) << 16);
     int wi = 0, ai = 0;
     uint32_t wph = 0, aph = 0;
+    T16Prof pf;
+    pf.start();
     for (int64_t u = u0; u < u1; u++) {
       mbar_wait(&wfull[wi], wph);
+      pf.lap(0);
       mbar_wait(&aempty[ai], aph ^ 1u);
+      pf.lap(1);
       tc16::fence_after();
       const uint8_t* raw = smem + C::kOffRaw + wi * C::kRaw + rgl * (kUnitBytes + kT16WsSlice);
       const uint4 w0 = lds128(raw + (r * 3 + 0) * 512 + lane * 16);
@@ -241,14 +259,17 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
           tc16::scale4(a[2 * h + 1], s1, v[4 * j + 2], v[4 * j + 3]);
         }
       }
+      pf.lap(2);
       tc16::st_16x256b_x8(tlane + C::kAcolBase + ai * 64, v);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc16::fence_before();
       __syncwarp();
       if (lane == 0) { tc16::arrive(&wempty[wi]); tc16::arrive(&afull[ai]); }
+      pf.lap(3);
       if (++wi == C::SW) { wi = 0; wph ^= 1u; }
       if (++ai == C::SA) { ai = 0; aph ^= 1u; }
     }
+    if (warp == 0 && lane == 0) pf.flush(p, 0, u1 - u0);
   } else if (warp == kT16WarpProdW) {
     // ===== weight producer: two T6 units and their two scale slices per k-block =====
     if (lane == 0) {
@@ -256,12 +277,13 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
       int wi = 0;
       uint32_t wph = 0;
       int64_t tile = u0 / kbn, kb = u0 - tile * kbn;
+      T16Prof pf;
+      pf.start();
       for (int64_t u = u0; u < u1; u++) {
         const int rg0 = (int)tile * 2;
         const int nu = rg0 + 1 < p.rg ? 2 : 1;
-        t16_mark(p, 2, u - u0, 0);
         mbar_wait(&wempty[wi], wph ^ 1u);
-        t16_mark(p, 2, u - u0, 1);
+        pf.lap(0);
         mbar_expect_tx(&wfull[wi], nu * (kUnitBytes + kT16WsSlice));
         uint8_t* dst = smem + C::kOffRaw + wi * C::kRaw;
         for (int j = 0; j < nu; j++) {
@@ -270,9 +292,11 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
           bulk_g2s(dst + j * (kUnitBytes + kT16WsSlice) + kUnitBytes,
                    p.wscale + ((int64_t)(rg0 + j) * kbn + kb) * kT16WsSlice, kT16WsSlice, &wfull[wi], pol);
         }
+        pf.lap(1);
         if (++wi == C::SW) { wi = 0; wph ^= 1u; }
         if (++kb == kbn) { kb = 0; tile++; }
       }
+      pf.flush(p, 1, u1 - u0);
     }
   } else if (warp == kT16WarpProdB) {
     // ===== activation producer: the fp16 B tile of each k-block (L2-resident) =====
@@ -282,15 +306,18 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
       int bi = 0;
       uint32_t bph = 0;
       int64_t kb = u0 % kbn;
+      T16Prof pf;
+      pf.start();
       for (int64_t u = u0; u < u1; u++) {
-        t16_mark(p, 3, u - u0, 0);
         mbar_wait(&aempty[bi], bph ^ 1u);
-        t16_mark(p, 3, u - u0, 1);
+        pf.lap(0);
         mbar_expect_tx(&afull[bi], C::kB);
         bulk_g2s(smem + C::kOffB + bi * C::kB, p.act + kb * (p.m_pad >> 3) * 2048, C::kB, &afull[bi], pol);
+        pf.lap(1);
         if (++bi == C::SA) { bi = 0; bph ^= 1u; }
         if (++kb == kbn) kb = 0;
       }
+      pf.flush(p, 2, u1 - u0);
     }
   } else if (warp == kT16WarpMma) {
     // ===== MMA issuer: 8 x (M=128, N=TN, K=16) per k-block into the tile's accumulator =====
@@ -298,14 +325,15 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
     uint32_t aph = 0, dph = 0;
     bool fresh = true;  // the next MMA starts a tile accumulator
     int64_t kb = u0 % kbn;
+    T16Prof pf;
+    pf.start();
     for (int64_t u = u0; u < u1; u++) {
       const bool tile_end = kb == kbn - 1 || u == u1 - 1;
       if (++kb == kbn) kb = 0;
-      if (lane == 0) t16_mark(p, 1, u - u0, 0);
       if (fresh) mbar_wait(&dempty[db], dph ^ 1u);
-      if (lane == 0) t16_mark(p, 1, u - u0, 1);
+      pf.lap(0);
       mbar_wait(&afull[ai], aph);
-      if (lane == 0) t16_mark(p, 1, u - u0, 2);
+      pf.lap(1);
       tc16::fence_after();
       if (lane == 0) {
         const uint32_t acol = tmem + C::kAcolBase + ai * 64;
@@ -316,13 +344,17 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
                            (fresh && s == 0) ? 0u : 1u);
         tc16::commit(&aempty[ai]);
         if (tile_end) tc16::commit(&dfull[db]);
-        t16_mark(p, 1, u - u0, 3);
       }
       __syncwarp();
+      pf.lap(2);
       fresh = tile_end;
-      if (tile_end) { db ^= 1; if (db == 0) dph ^= 1u; }
+      if (tile_end) {
+        if (C::NACC == 2) { db ^= 1; if (db == 0) dph ^= 1u; }
+        else dph ^= 1u;
+      }
       if (++ai == C::SA) { ai = 0; aph ^= 1u; }
     }
+    if (lane == 0) pf.flush(p, 3, u1 - u0);
   } else {
     // ===== epilogue: per tile, fp32 accumulator -> fp16 y (or the stream-K fixup) =====
     const int q = warp & 3;  // TMEM lane quarter
@@ -365,8 +397,8 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
       tc16::fence_before();
       __syncwarp();
       if (lane == 0) tc16::arrive(&dempty[db]);  // the MMA may refill this accumulator
-      db ^= 1;
-      if (db == 0) dph ^= 1u;
+      if (C::NACC == 2) { db ^= 1; if (db == 0) dph ^= 1u; }
+      else dph ^= 1u;
       if (split) {
         __threadfence();
         tc16::named_sync(1, kT16EpiWarps * 32);
@@ -420,17 +452,17 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
 // ---- host side ------------------------------------------------------------------------------
 static long long* g_t16_tl = nullptr;
 extern "C" int flexq_debug_tc16_timeline(long long* host, int max_entries) {
-  const int n = 4 * kT16TlUnits * 4;
+  const int n = 4 * 8;
   if (!g_t16_tl || max_entries < n) return 0;
   cudaDeviceSynchronize();
   cudaMemcpy(host, g_t16_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
   return n;
 }
 
-static int t16_tn(int64_t m) { return m <= 32 ? 32 : m <= 64 ? 64 : 128; }
+static int t16_tn(int64_t m) { return m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 256; }
 
 bool gemm_tc16_supported(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f16) {
-  return m > 16 && m <= 128 && gs == 128 && k % 128 == 0 && scale_f16 && n >= 1;
+  return m > 16 && m <= 256 && gs == 128 && k % 128 == 0 && scale_f16 && n >= 1;
 }
 
 int64_t gemm_tc16_act_bytes(int64_t m, int64_t k) {
@@ -459,7 +491,7 @@ int gemm_tc16_launch(const uint32_t* t6, const void* wscale, const void* act_f16
                      int64_t n, int64_t k, void* y, int out_dtype, void* workspace,
                      const void* residual, cudaStream_t st) {
   if (!gemm_tc16_supported(m, n, k, 128, 1) || !workspace || !y) {
-    set_error("gemm_tc16: needs 16 < m <= 128, group 128, fp16 scales, K %% 128 == 0, a workspace");
+    set_error("gemm_tc16: needs 16 < m <= 256, group 128, fp16 scales, K %% 128 == 0, a workspace");
     return FLEXQ_ERR_CONFIG;
   }
   T6Geom G(n, k, 128);
@@ -484,14 +516,15 @@ int gemm_tc16_launch(const uint32_t* t6, const void* wscale, const void* act_f16
   p.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) +
                                            cdiv(s2 * 2 * tn * 128 * 4, 256) * 256);
   if (tuning().tc_timeline) {
-    if (!g_t16_tl) cudaMalloc(&g_t16_tl, 4 * kT16TlUnits * 4 * sizeof(long long));
-    cudaMemsetAsync(g_t16_tl, 0, 4 * kT16TlUnits * 4 * sizeof(long long), st);
+    if (!g_t16_tl) cudaMalloc(&g_t16_tl, 4 * 8 * sizeof(long long));
+    cudaMemsetAsync(g_t16_tl, 0, 4 * 8 * sizeof(long long), st);
     p.tl = g_t16_tl;
   }
   const bool f32 = out_dtype == FLEXQ_OUT_F32;
   switch (tn) {
     case 32: return f32 ? launch_tc16_inst<32, FLEXQ_OUT_F32>(p, st) : launch_tc16_inst<32, FLEXQ_OUT_F16>(p, st);
     case 64: return f32 ? launch_tc16_inst<64, FLEXQ_OUT_F32>(p, st) : launch_tc16_inst<64, FLEXQ_OUT_F16>(p, st);
+    case 256: return f32 ? launch_tc16_inst<256, FLEXQ_OUT_F32>(p, st) : launch_tc16_inst<256, FLEXQ_OUT_F16>(p, st);
     default: return f32 ? launch_tc16_inst<128, FLEXQ_OUT_F32>(p, st) : launch_tc16_inst<128, FLEXQ_OUT_F16>(p, st);
   }
 }

@@ -27,19 +27,20 @@ def main():
     L = _lib.lib()
     fn = L.flexq_debug_tc16_timeline
     fn.restype = ctypes.c_int
-    buf = (ctypes.c_longlong * (4 * 64 * 4))()
-    fn(buf, 4 * 64 * 4)
-    a = np.frombuffer(buf, dtype=np.int64).reshape(4, 64, 4)
-    names = ["conv(start,wfull,aempty,done)", "mma(start,dempty,afull,issued)",
-             "wprod(start,wempty,-,-)", "bprod(start,aempty,-,-)"]
-    for r, nm in enumerate(names):
-        rows = a[r, 8:]
-        rows = rows[rows[:, 0] > 0]
-        if len(rows) < 3:
-            continue
-        per = np.median(np.diff(rows[:, 0]))
-        gaps = [np.median(rows[:, e + 1] - rows[:, e]) for e in range(3) if (rows[:, e + 1] > 0).all()]
-        print(f"{nm:40s} period {per:7.0f}  gaps " + " ".join(f"{g:7.0f}" for g in gaps))
+    buf = (ctypes.c_longlong * 32)()
+    if fn(buf, 32) == 0:
+        print("no profile: build with -DFLEXQ_TC16_TIMELINE=1 (tools/build_debug.sh) and set FLEXQ_LIB")
+        return
+    a = np.frombuffer(buf, dtype=np.int64).reshape(4, 8)
+    roles = [("converter w0", ["wait raw", "wait A/B stage", "convert", "store+arrive"]),
+             ("weight producer", ["wait free raw", "issue"]),
+             ("B producer", ["wait free stage", "issue"]),
+             ("MMA", ["wait TMEM acc", "wait operands", "issue+commit"])]
+    for r, (name, phases) in enumerate(roles):
+        units = max(int(a[r, 4]), 1)
+        tot = sum(a[r, :len(phases)])
+        print(f"{name:16s} {units} units, {tot / units:7.0f} cyc/unit: " +
+              ", ".join(f"{ph} {a[r, i] / units:6.0f}" for i, ph in enumerate(phases)))
 
 
 if __name__ == "__main__":
