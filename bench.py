@@ -383,15 +383,14 @@ def main():
     except Exception:
         pass
     launches_per_fwd = 2  # fused activation quantizer + one GEMV/GEMM kernel per linear
-    # the automatic route (csrc/gemm_t6.cu): streaming GEMV for M <= 16, and for M <= 32 on
-    # layers of >= 8192 units (64 rows x 128 k); tcgen05 otherwise
-    streamed = [M <= 16 or (M <= 32 and -(-lay.n // 64) * -(-lay.k // 128) >= 8192) for _, lay in layers]
-    kern_gemv = "flexq::gemv_t6_stream_kernel"
-    kern_tc = "flexq::gemm_tc_kernel (tcgen05.mma kind::i8)"
-    kernel_label = kern_gemv if all(streamed) else kern_tc if not any(streamed) else \
-        f"{kern_gemv} + {kern_tc}"
-    dtype_label = ("int8 IMMA mma.sync" if all(streamed) else "int8 tcgen05.mma kind::i8"
-                   if not any(streamed) else "int8 IMMA mma.sync + tcgen05.mma kind::i8")
+    # the kernel flexq_linear_forward routes each layer to (flexq_linear_kernel)
+    names = {_lib.KERNEL_GEMV: ("flexq::gemv_t6_stream_kernel", "int8 IMMA mma.sync (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue"),
+             _lib.KERNEL_TC_I8: ("flexq::gemm_tc_kernel (tcgen05.mma kind::i8)", "int8 tcgen05.mma kind::i8 (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue"),
+             _lib.KERNEL_TC16: ("flexq::gemm_tc16_kernel (tcgen05.mma kind::f16)", "tcgen05.mma kind::f16 over fp16(w*ws) x fp16(code*xs) (INT6/INT8 codes, fp16 scales), fp32 accum"),
+             _lib.KERNEL_MMA_SYNC: ("flexq::gemm_t6_kernel (mma.sync)", "int8 IMMA mma.sync, int32 accum")}
+    kinds = sorted({_lib.lib().flexq_linear_kernel(M, lay.n, lay.k, 128, 1) for _, lay in layers})
+    kernel_label = " + ".join(names[k_][0] for k_ in kinds)
+    dtype_label = " + ".join(names[k_][1] for k_ in kinds)
     desc = (f"{args.model} decoder-layer linears qkv,o,gate,up (W6A6) + down (W6A8), M={M}"
             if args.model in MODELS else WORKLOAD_DESC.get(args.model, args.model) + f", M={M}")
     wbytes = sum(lay.weight_bytes for _, lay in layers) * world
@@ -399,7 +398,7 @@ def main():
         "metric": METRIC, "value": tops, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": dtype_label + " (u6 offset-binary W x s8 A), int32 accum, fp32 epilogue, fp16 out",
+        "dtype": dtype_label + ", fp16 out",
         "data": "synthetic: random-init INT6 weights of the real shapes (fp16 N(0,1) quantized), fp16 N(0,1) activations",
         "config": {"workload": desc, "batch": M, "group_size": 128, "scales": "fp16",
                    "parallelism": (f"tp{world}: qkv/gate/up column shards + NCCL all-gather, "

@@ -355,6 +355,9 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
       if (++ai == C::SA) { ai = 0; aph ^= 1u; }
     }
     if (lane == 0) pf.flush(p, 3, u1 - u0);
+    if constexpr (FLEXQ_TC16_TIMELINE) {  // every CTA: its MMA loop's total cycles
+      if (lane == 0 && p.tl) p.tl[32 + blockIdx.x] = pf.acc[0] + pf.acc[1] + pf.acc[2];
+    }
   } else {
     // ===== epilogue: per tile, fp32 accumulator -> fp16 y (or the stream-K fixup) =====
     const int q = warp & 3;  // TMEM lane quarter
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
 // ---- host side ------------------------------------------------------------------------------
 static long long* g_t16_tl = nullptr;
 extern "C" int flexq_debug_tc16_timeline(long long* host, int max_entries) {
-  const int n = 4 * 8;
+  const int n = 32 + 1024;
   if (!g_t16_tl || max_entries < n) return 0;
   cudaDeviceSynchronize();
   cudaMemcpy(host, g_t16_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -516,8 +519,8 @@ int gemm_tc16_launch(const uint32_t* t6, const void* wscale, const void* act_f16
   p.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) +
                                            cdiv(s2 * 2 * tn * 128 * 4, 256) * 256);
   if (tuning().tc_timeline) {
-    if (!g_t16_tl) cudaMalloc(&g_t16_tl, 4 * 8 * sizeof(long long));
-    cudaMemsetAsync(g_t16_tl, 0, 4 * 8 * sizeof(long long), st);
+    if (!g_t16_tl) cudaMalloc(&g_t16_tl, (32 + 1024) * sizeof(long long));
+    cudaMemsetAsync(g_t16_tl, 0, (32 + 1024) * sizeof(long long), st);
     p.tl = g_t16_tl;
   }
   const bool f32 = out_dtype == FLEXQ_OUT_F32;

@@ -27,11 +27,17 @@ def main():
     L = _lib.lib()
     fn = L.flexq_debug_tc16_timeline
     fn.restype = ctypes.c_int
-    buf = (ctypes.c_longlong * 32)()
-    if fn(buf, 32) == 0:
+    buf = (ctypes.c_longlong * (32 + 1024))()
+    if fn(buf, 32 + 1024) == 0:
         print("no profile: build with -DFLEXQ_TC16_TIMELINE=1 (tools/build_debug.sh) and set FLEXQ_LIB")
         return
-    a = np.frombuffer(buf, dtype=np.int64).reshape(4, 8)
+    allv = np.frombuffer(buf, dtype=np.int64)
+    a = allv[:32].reshape(4, 8)
+    per = allv[32:32 + 1024]
+    per = per[per > 0]
+    if len(per):
+        print(f"MMA loop cycles over {len(per)} CTAs: min {per.min()} median {int(np.median(per))} "
+              f"max {per.max()} (CTA 0: {per[0]})")
     roles = [("converter w0", ["wait raw", "wait A/B stage", "convert", "store+arrive"]),
              ("weight producer", ["wait free raw", "issue"]),
              ("B producer", ["wait free stage", "issue"]),
