@@ -196,8 +196,8 @@ def test_fused_residual_epilogue(m):
     (64, 1000, 4096, 6),      # N not a multiple of 128, split tiles
     (100, 640, 8192, 8),      # tile 128, deep stream-K
     (128, 384, 28672, 8),     # down_proj K: 224 k-blocks
-    (129, 512, 4096, 6),      # N = 256 token tile (single accumulator)
-    (256, 1000, 8192, 8),     # M = 256, N not a multiple of 128
+    (129, 8200, 8192, 6),     # 256-token tile (single accumulator); >= 8192 units to take it
+    (256, 8192, 8192, 8),     # M = 256
 ])
 def test_tc16_fast_path(m, n, k, q):
     """The batched fast path (csrc/gemm_tc16.cu: tcgen05 kind::f16 over fp16(w*ws) and
