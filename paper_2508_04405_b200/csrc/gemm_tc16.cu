@@ -57,6 +57,35 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One k-block's 8 MMAs (K = 16 each, A columns +8 and B descriptor +16 per step) and the
+// commit of the A slot, issued by the whole converged warp through one elect.sync inside a
+// single asm block (B descriptor +16 = +256 B per K = 16 step): the operands are converted to uniform registers once per k-block instead of
+// once per instruction inside a per-MMA elect loop (tools/probe/umma_factors.cu).
+__device__ __forceinline__ void mma8_commit(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate, uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e, p, t;\n.reg .b32 a;\n.reg .b64 b;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "add.u32 a, %1, 8;\nadd.u64 b, %2, 16;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+      "add.u32 a, %1, 16;\nadd.u64 b, %2, 32;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+      "add.u32 a, %1, 24;\nadd.u64 b, %2, 48;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+      "add.u32 a, %1, 32;\nadd.u64 b, %2, 64;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+      "add.u32 a, %1, 40;\nadd.u64 b, %2, 80;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+      "add.u32 a, %1, 48;\nadd.u64 b, %2, 96;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+      "add.u32 a, %1, 56;\nadd.u64 b, %2, 112;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar))
+      : "memory");
+}
 // 16 TMEM lanes x 64 columns from one warp: thread t's registers 4j..4j+3 land in
 // (lane t/4, columns 8j + 2(t%4), +1) and (lane 8 + t/4, same columns) -- measured,
 // tools/probe/tmem_layout.cu
@@ -335,16 +364,11 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
       mbar_wait(&afull[ai], aph);
       pf.lap(1);
       tc16::fence_after();
-      if (lane == 0) {
-        const uint32_t acol = tmem + C::kAcolBase + ai * 64;
-        const uint64_t bd = tc16::desc_b(smem_u32(smem + C::kOffB + ai * C::kB));
-#pragma unroll
-        for (int s = 0; s < 8; s++)
-          tc16::mma_f16_ts(tmem + db * TN, acol + 8 * s, bd + (uint64_t)(s * 16), C::kIdesc,
-                           (fresh && s == 0) ? 0u : 1u);
-        tc16::commit(&aempty[ai]);
-        if (tile_end) tc16::commit(&dfull[db]);
-      }
+      __syncwarp();
+      tc16::mma8_commit(tmem + db * TN, tmem + C::kAcolBase + ai * 64,
+                        tc16::desc_b(smem_u32(smem + C::kOffB + ai * C::kB)), C::kIdesc,
+                        fresh ? 0u : 1u, &aempty[ai]);
+      if (lane == 0 && tile_end) tc16::commit(&dfull[db]);
       __syncwarp();
       pf.lap(2);
       fresh = tile_end;
