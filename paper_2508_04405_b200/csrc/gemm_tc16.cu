@@ -151,8 +151,8 @@ __device__ __forceinline__ void scale4(uint32_t word, __half2 s2, uint32_t& lo, 
 }  // namespace tc16
 
 constexpr int kT16ConvWarps = 8, kT16WarpProdW = 8, kT16WarpMma = 9, kT16WarpProdB = 10,
-              kT16WarpEpi0 = 11, kT16EpiWarps = 4;
-constexpr int kT16Threads = (kT16WarpEpi0 + kT16EpiWarps) * 32;
+              kT16WarpEpi0 = 11, kT16EpiWarps = 4, kT16WarpProdW2 = 15;
+constexpr int kT16Threads = 16 * 32;
 constexpr int kT16WsSlice = kRowGroup * 8 * 4;  // fp16 scale pairs of one row group and group
 
 template <int TN>
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
   const int kbn = p.kbn;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C::SW; i++) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], kT16ConvWarps); }
+    for (int i = 0; i < C::SW; i++) { mbar_init(&wfull[i], 2); mbar_init(&wempty[i], kT16ConvWarps); }
     for (int i = 0; i < C::SA; i++) { mbar_init(&afull[i], kT16ConvWarps + 1); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < 2; i++) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], kT16EpiWarps); }
     fence_mbar_init();
@@ -299,8 +299,11 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
       if (++ai == C::SA) { ai = 0; aph ^= 1u; }
     }
     if (warp == 0 && lane == 0) pf.flush(p, 0, u1 - u0);
-  } else if (warp == kT16WarpProdW) {
-    // ===== weight producer: two T6 units and their two scale slices per k-block =====
+  } else if (warp == kT16WarpProdW || warp == kT16WarpProdW2) {
+    // ===== weight producers: one per row group of the tile, a T6 unit and its scale slice per
+    // k-block each (two issuing threads: one thread's bulk copies stream measurably slower,
+    // tools/probe/stream.cu) =====
+    const int pj = warp == kT16WarpProdW ? 0 : 1;
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       int wi = 0;
@@ -313,9 +316,9 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
         const int nu = rg0 + 1 < p.rg ? 2 : 1;
         mbar_wait(&wempty[wi], wph ^ 1u);
         pf.lap(0);
-        mbar_expect_tx(&wfull[wi], nu * (kUnitBytes + kT16WsSlice));
+        mbar_expect_tx(&wfull[wi], pj < nu ? kUnitBytes + kT16WsSlice : 0);
         uint8_t* dst = smem + C::kOffRaw + wi * C::kRaw;
-        for (int j = 0; j < nu; j++) {
+        for (int j = pj; j < nu && j == pj; j++) {
           bulk_g2s(dst + j * (kUnitBytes + kT16WsSlice), p.t6 + ((int64_t)(rg0 + j) * kbn + kb) * kUnitBytes,
                    kUnitBytes, &wfull[wi], pol);
           bulk_g2s(dst + j * (kUnitBytes + kT16WsSlice) + kUnitBytes,
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
         if (++wi == C::SW) { wi = 0; wph ^= 1u; }
         if (++kb == kbn) { kb = 0; tile++; }
       }
-      pf.flush(p, 1, u1 - u0);
+      if (pj == 0) pf.flush(p, 1, u1 - u0);
     }
   } else if (warp == kT16WarpProdB) {
     // ===== activation producer: the fp16 B tile of each k-block (L2-resident) =====
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
     if constexpr (FLEXQ_TC16_TIMELINE) {  // every CTA: its MMA loop's total cycles
       if (lane == 0 && p.tl) p.tl[32 + blockIdx.x] = pf.acc[0] + pf.acc[1] + pf.acc[2];
     }
-  } else {
+  } else if (warp >= kT16WarpEpi0 && warp < kT16WarpEpi0 + kT16EpiWarps) {
     // ===== epilogue: per tile, fp32 accumulator -> fp16 y (or the stream-K fixup) =====
     const int q = warp & 3;  // TMEM lane quarter
     const int rho = 32 * q + lane;
