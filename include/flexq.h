@@ -180,6 +180,12 @@ int flexq_group_epilogue_f64(const int32_t* partials, const double* wscale,
 #define FLEXQ_KERNEL_MMA_SYNC 3  /* mma.sync (group sizes not aligned to 128 k) */
 /* The GEMM kernel flexq_linear_forward uses for this shape (the FLEXQ_KERNEL_* codes). */
 int flexq_linear_kernel(int64_t m, int64_t n, int64_t k, int64_t group_size, int scale_f16);
+/* Process-wide override of the kind::f16 route for 32 < M <= 256 (A/B runs and tests that cover
+ * the kernel on small shapes): -1 = automatic (measured size rule, the default), 0 = never,
+ * 1 = whenever gemm_tc16 supports the shape.  Returns the previous mode, or -2 (and sets the
+ * error string) for an invalid mode.  No reference counterpart: routing is internal to this
+ * library (the reference has one CPU path, engine.py:290). */
+int flexq_set_tc16_route(int mode);
 int flexq_gemm_tc16(const uint32_t* t6, const void* wscale, const void* act_f16, int64_t m,
                     int64_t n, int64_t k, void* y, int out_dtype, void* workspace,
                     const void* residual, cudaStream_t stream);

@@ -52,6 +52,7 @@ SIGNATURES = {
     "flexq_linear_forward_ex": (i32, [vp, vp, i32, i32, vp, i64, i64, i64, i64, vp, i32, vp, vp, vp,
                                       vp, vp]),
     "flexq_linear_kernel": (i32, [i64, i64, i64, i64, i32]),
+    "flexq_set_tc16_route": (i32, [i32]),
     "flexq_gemm_tc16": (i32, [vp, vp, vp, i64, i64, i64, vp, i32, vp, vp, vp]),
     "flexq_act_f16_operand": (vp, [vp, i64, i64, i64]),
     "flexq_rmsnorm_quantize": (i32, [vp, i64, vp, ctypes.c_float, i64, i64, i32, i64, vp, vp, vp,

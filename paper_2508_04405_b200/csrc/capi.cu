@@ -1,6 +1,7 @@
 // extern "C" boundary of libflexq_sm100a.so (declared in include/flexq.h).
 // Argument validation here mirrors the reference's raising sites so the
 // Python wrapper can map status codes to the same exception classes.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -327,13 +328,29 @@ int64_t flexq_act_m_pad(int64_t m) { return m < 1 ? 0 : tc_act_m_pad(m); }
 
 // The batched forward takes the kind::f16 kernel (gemm_tc16.cu) for 32 < m <= 128 at group 128
 // with fp16 weight scales; the fp16 operand then follows the INT8 operand in the act buffer.
+static std::atomic<int> g_tc16_mode{-1};  // flexq_set_tc16_route: -1 auto, 0 never, 1 always
+
 static bool tc16_route(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f16) {
   if (m <= 32 || tuning().disable_tc16 || tuning().disable_tc || !gemm_tc16_supported(m, n, k, gs, scale_f16))
     return false;
-  // 128 < M <= 256 (one 256-token tile, a single TMEM accumulator): faster than the INT8
-  // kernel on layers of >= 8192 units (70B gate 122 vs 186 us), not on smaller ones
-  // (70B qkv 82 vs 79 us; tools/ab_tc16.sh)
-  return m <= 128 || cdiv(n, 64) * cdiv(k, 128) >= 8192;
+  const int mode = g_tc16_mode.load(std::memory_order_relaxed);
+  if (mode >= 0) return mode == 1;
+  // Measured A/B against the INT8 kernel (tools/ab_tc16.sh, LLaMA-2 7B/13B/70B linears):
+  // kind::f16 wins on layers of >= 8192 units (70B gate M = 64/128/256: 60/73/118 vs
+  // 85/103/187 us) and loses on smaller ones (7B q_proj M = 128: 40 vs 31 us: too few k-blocks
+  // per CTA to fill its deeper pipeline).  For 128 < M <= 256 (one 256-token tile) it also
+  // needs a wide or long layer (13B down_proj 5120 x 13824 M = 256: 82 vs 68 us).
+  const int64_t units = cdiv(n, 64) * cdiv(k, 128);
+  if (units < 8192) return false;
+  return m <= 128 || n >= 10240 || units >= 16384;
+}
+
+int flexq_set_tc16_route(int mode) {
+  if (mode < -1 || mode > 1) {
+    set_error("set_tc16_route: mode must be -1 (auto), 0 (never) or 1 (always)");
+    return -2;
+  }
+  return g_tc16_mode.exchange(mode);
 }
 
 static int64_t act_f16_offset(int64_t m, int64_t k, int64_t group_size) {

@@ -77,3 +77,22 @@ def test_product_path_has_no_cpu_fallback():
         fq.quantize(np.ones((2, 128)), 6)
     with pytest.raises(fq.DeviceError):
         fq.quantized_linear(np.ones((8, 128)), np.ones((1, 128)))
+
+
+def test_tc16_route_rule_and_override():
+    """The kind::f16 batched route: measured size rule by default (>= 8192 units; 128 < M <=
+    256 only on wide or long layers), a process-wide override for A/B runs and tests."""
+    L = _lib.load()  # host-only: routing needs no device
+    assert L.flexq_set_tc16_route(5) == -2  # invalid mode: rejected, state unchanged
+    prev = L.flexq_set_tc16_route(-1)
+    try:
+        assert L.flexq_linear_kernel(64, 28672, 8192, 128, 1) == _lib.KERNEL_TC16   # 70B gate
+        assert L.flexq_linear_kernel(256, 28672, 8192, 128, 1) == _lib.KERNEL_TC16  # wide
+        assert L.flexq_linear_kernel(256, 8192, 28672, 128, 1) == _lib.KERNEL_TC16  # long
+        assert L.flexq_linear_kernel(64, 4096, 4096, 128, 0) != _lib.KERNEL_TC16    # fp32 scales
+        assert L.flexq_set_tc16_route(1) == -1
+        assert L.flexq_linear_kernel(64, 4096, 4096, 128, 1) == _lib.KERNEL_TC16    # forced
+        assert L.flexq_linear_kernel(64, 4096, 4096, 64, 1) != _lib.KERNEL_TC16     # unsupported
+        assert L.flexq_set_tc16_route(-1) == 1
+    finally:
+        L.flexq_set_tc16_route(prev)

@@ -205,6 +205,14 @@ def test_tc16_fast_path(m, n, k, q):
     fp16 y within max|y - y_ref| <= 1e-3 * max|y_ref| of int_matmul_reference (engine.py:
     337-365); gemm_only replays the identical output; run to run bit-identical."""
     L = _lib.lib()
+    prev = L.flexq_set_tc16_route(1)  # small shapes: the size rule would pick kind::i8
+    try:
+        _tc16_case(L, m, n, k, q)
+    finally:
+        L.flexq_set_tc16_route(prev)
+
+
+def _tc16_case(L, m, n, k, q):
     assert L.flexq_linear_kernel(m, n, k, 128, 1) == _lib.KERNEL_TC16
     w, x, _, y_ref, _ = case(m, n, k, q, 128, seed=17 * m + n)
     lin = fq.FlexQLinear(w, activation_bits=q)

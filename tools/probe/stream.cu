@@ -169,11 +169,22 @@ void multi_case(const uint8_t* buf, const uint8_t* side, size_t bytes, unsigned*
   run(name, [&] { tma_multi<S, CH, NS, SM><<<148 * cps, wpc * 32, smem>>>(buf, side, bytes, nw, out, wpc); }, bytes / CH * CH);
 }
 
-int main() {
+int main(int argc, char** argv) {
   size_t bytes = (size_t)1 << 30;
   uint8_t* buf; cudaMalloc(&buf, bytes); cudaMemset(buf, 1, bytes);
   unsigned* out; cudaMalloc(&out, 64);
   uint8_t* side; cudaMalloc(&side, 4096 * 1024); cudaMemset(side, 2, 4096 * 1024);
+  if (argc > 1) {  // one issuing thread per SM (the tcgen05 kernels' weight producer)
+    tma_case<8, 12288>(buf, bytes, out, 1, 1);
+    tma_case<14, 12288>(buf, bytes, out, 1, 1);
+    tma_case<7, 24576>(buf, bytes, out, 1, 1);
+    tma_case<16, 6144>(buf, bytes, out, 1, 1);
+    tma_case<28, 6144>(buf, bytes, out, 1, 1);
+    tma_case<7, 12288>(buf, bytes, out, 2, 1);
+    tma_case<4, 12288>(buf, bytes, out, 4, 1);
+    tma_case<3, 6144>(buf, bytes, out, 4, 2);
+    return 0;
+  }
   multi_case<2, 6144, 0, 16>(buf, side, bytes, out, 4, 3);
   multi_case<2, 6144, 1, 1024>(buf, side, bytes, out, 4, 3);
   multi_case<2, 6144, 4, 32>(buf, side, bytes, out, 4, 3);
