@@ -446,11 +446,26 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
             float a[16];
 #pragma unroll
             for (int j = 0; j < 16; j++) a[j] = 0.f;
-            for (int64_t cc = first_c; cc <= last_c; cc++) {  // fixed CTA order: deterministic
-              const int wc = t16_start(cc, U, P) >= tile * kbn ? 0 : 1;
-              const float* src = p.ws_part + ((cc * 2 + wc) * TN + c0) * (int64_t)128 + rho;
+            // contributors in fixed CTA order (deterministic), four per L2 round trip: the
+            // loads of a batch are all issued before the ordered sum consumes them
+            for (int64_t cb = first_c; cb <= last_c; cb += 4) {
+              float v[4][16];
 #pragma unroll
-              for (int j = 0; j < 16; j++) a[j] += __ldcg(src + j * 128);
+              for (int b = 0; b < 4; b++) {
+                const int64_t cc = cb + b;
+                if (cc <= last_c) {
+                  const int wc = t16_start(cc, U, P) >= tile * kbn ? 0 : 1;
+                  const float* src = p.ws_part + ((cc * 2 + wc) * TN + c0) * (int64_t)128 + rho;
+#pragma unroll
+                  for (int j = 0; j < 16; j++) v[b][j] = __ldcg(src + j * 128);
+                }
+              }
+#pragma unroll
+              for (int b = 0; b < 4; b++)
+                if (cb + b <= last_c) {
+#pragma unroll
+                  for (int j = 0; j < 16; j++) a[j] += v[b][j];
+                }
             }
             if (n_row < p.n) {
 #pragma unroll
