@@ -27,7 +27,7 @@ def main(tag):
     out += ["## bench.py (LLaMA-2-70B decoder-layer linears, CUDA-graph step)", "",
             "| M | value (TOPS) | us/step | GEMM GB/s | roofline frac (of measured HBM) | e2e TOPS | CPU baseline TOPS (cores) | SM MHz |",
             "|---|---|---|---|---|---|---|---|"]
-    for m in ("m1", "m8", "m32", "m128"):
+    for m in ("m1", "m8", "m32", "m64", "m128", "m256"):
         p = os.path.join(src, f"{tag}_bench_{m}.json")
         if not os.path.exists(p):
             continue

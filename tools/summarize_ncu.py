@@ -80,7 +80,10 @@ def summarize(tag: str, model: str):
         if not os.path.exists(rep):
             continue
         rows = raw_rows(rep)
-        kname = "gemv_t6_stream_kernel" if m <= 32 else "gemm_tc_kernel (tcgen05.mma kind::i8)"
+        names = sorted({(r.get("Kernel Name") or "?").split("(")[0] for r in rows})
+        kname = " / ".join(names) + {"gemm_tc_kernel": " (tcgen05.mma kind::i8)",
+                                     "flexq::gemm_tc16_kernel": " (tcgen05.mma kind::f16)"}.get(
+                                         names[0].split("<")[0] if len(names) == 1 else "", "")
         lines += [f"## M={m}: `ncu --set full` on the {len(rows)} {kname} launches of one step", "",
                   "| layer | " + " | ".join(lbl for _, lbl in KEYS) + " |",
                   "|---" * (len(KEYS) + 1) + "|"]

@@ -26,10 +26,15 @@ sys.path.insert(0, ROOT)
 L2_BYTES = 126 * 2**20
 
 
+_KERNELS = {0: "gemv_stream", 1: "gemm_tc", 2: "gemm_tc16", 3: "gemm_t6"}
+
+
 def kernel_name(m, n, k):
-    """The automatic route of flexq_gemm_t6 at group 128 (csrc/gemm_t6.cu, gemv_stream.cu)."""
-    units = -(-n // 64) * -(-k // 128)
-    return "gemv_stream" if m <= 16 or (m <= 32 and units >= 8192) else "gemm_tc"
+    """The kernel flexq_linear_forward routes this shape to at group 128, fp16 scales
+    (flexq_linear_kernel: csrc/capi.cu)."""
+    from paper_2508_04405_b200 import _lib
+
+    return _KERNELS.get(_lib.load().flexq_linear_kernel(m, n, k, 128, 1), "?")
 
 
 def main():
