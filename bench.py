@@ -365,6 +365,12 @@ def main():
         e2e_step()
     ms_e2e = st.timed(e2e_step, args.e2e_steps)
 
+    def eager_step():  # diagnostic: the same eager forwards without the host copies
+        for i, (s, lay) in enumerate(layers):
+            lay(in_views[s.k] if world == 1 else dev_in[s.k], out=out_views[i] if world == 1 else None)
+
+    ms_eager = st.timed(eager_step, args.e2e_steps) if world == 1 else None
+
     from paper_2508_04405_b200.shapes import gemm_bytes
 
     flops_total = sum(2 * M * s.n * s.k for s in shapes)  # whole job (all ranks)
@@ -420,7 +426,8 @@ def main():
         "clocks": clk.summary(),
         "e2e": {"value": flops_total / (ms_e2e * 1e-3) / 1e12, "unit": "TOPS",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": ms_e2e, "path": "FlexQLinear.__call__ (public API); per step one H2D of the inputs from pinned host memory and one D2H of all outputs"},
+                "ms_per_step": ms_e2e, "ms_per_step_eager_no_copies": ms_eager,
+                "path": "FlexQLinear.__call__ (public API); per step one H2D of the inputs from pinned host memory and one D2H of all outputs"},
         "gpu_launches": args.steps * len(shapes) * launches_per_fwd,
         "tuning": _lib.lib().flexq_tuning().decode(),
     }

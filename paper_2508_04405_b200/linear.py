@@ -55,6 +55,7 @@ class FlexQLinear:
         self.t6, self.wscale = t6_pack_weights(codes, scales, self.k, self.group_size,
                                                scale_f16=self.fp16_scales)
         self.device = codes.device
+        self._dev_index = codes.device.index if codes.device.index is not None else 0
         self._bufs: dict[int, tuple] = {}
         self._f16_ready: set[int] = set()  # batches whose act buffer holds the fp16 operand
         self.flag = t.zeros(1, dtype=t.int32, device=self.device)
@@ -134,7 +135,7 @@ class FlexQLinear:
         buffers of a stream that already ran this batch eagerly, so the graph's replays and
         eager forwards on that stream must be stream-ordered."""
         t = _dev.torch()
-        key = (m, _lib.stream() if stream is None else stream)
+        key = (m, _lib.stream(self._dev_index) if stream is None else stream)
         if key not in self._bufs:
             if t.cuda.is_current_stream_capturing():
                 for (mm, _), bufs in self._bufs.items():
@@ -192,15 +193,19 @@ class FlexQLinear:
             self._check_out("out", out, m, out_dtype)
         if residual is not None:
             self._check_out("residual", residual, m, out_dtype)
-        act, ws = self.buffers(m)
-        if _lib.lib().flexq_linear_kernel(m, self.n, self.k, self.group_size,
-                                          int(self.fp16_scales)) == _lib.KERNEL_TC16:
+        st = _lib.stream(self._dev_index)
+        act, ws = self.buffers(m, st)
+        L = _lib.lib()
+        if L.flexq_linear_kernel(m, self.n, self.k, self.group_size,
+                                 int(self.fp16_scales)) == _lib.KERNEL_TC16:
             self._f16_ready.add(m)
-        _lib.check(_lib.lib().flexq_linear_forward_ex(
-            _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), self.activation_bits,
-            _lib.ptr(x), m, self.n, self.k, self.group_size, _lib.ptr(out),
-            _lib.OUT_F32 if out_dtype == t.float32 else _lib.OUT_F16, _lib.ptr(act),
-            _lib.ptr(ws), _lib.ptr(self.flag), _lib.ptr(residual), _lib.stream()))
+        else:  # the route can change (flexq_set_tc16_route): gemm_only follows the last forward
+            self._f16_ready.discard(m)
+        _lib.check(L.flexq_linear_forward_ex(
+            self.t6.data_ptr(), self.wscale.data_ptr(), int(self.fp16_scales), self.activation_bits,
+            x.data_ptr(), m, self.n, self.k, self.group_size, out.data_ptr(),
+            _lib.OUT_F32 if out_dtype == t.float32 else _lib.OUT_F16, act.data_ptr(),
+            ws.data_ptr(), self.flag.data_ptr(), _lib.ptr(residual), st))
         return out
 
     __call__ = forward
@@ -234,14 +239,14 @@ class FlexQLinear:
             _lib.check(L.flexq_gemm_tc16(
                 _lib.ptr(self.t6), _lib.ptr(self.wscale), op, m, self.n, self.k, _lib.ptr(out),
                 _lib.OUT_F32 if out.dtype == t.float32 else _lib.OUT_F16, _lib.ptr(ws),
-                _lib.ptr(residual), _lib.stream()))
+                _lib.ptr(residual), _lib.stream(self._dev_index)))
             return out
         frag, xs, corr, m_pad = self._act_views(m)
         _lib.check(_lib.lib().flexq_gemm_t6_ex(
             _lib.ptr(self.t6), _lib.ptr(self.wscale), int(self.fp16_scales), frag, xs, corr, m,
             m_pad, self.n, self.k, self.group_size, None, _lib.ptr(out),
             _lib.OUT_F32 if out.dtype == t.float32 else _lib.OUT_F16,
-            _lib.ptr(ws), 0, _lib.ptr(residual), _lib.stream()))
+            _lib.ptr(ws), 0, _lib.ptr(residual), _lib.stream(self._dev_index)))
         return out
 
     def check_errors(self) -> None:
