@@ -95,6 +95,9 @@ const Tuning& tuning() {
     }
     if (env("FLEXQ_MIN_UNITS") && atoi(env("FLEXQ_MIN_UNITS")) > 0)
       v.min_units = atoi(env("FLEXQ_MIN_UNITS"));
+    if (env("FLEXQ_TC_MIN_UNITS") && atoi(env("FLEXQ_TC_MIN_UNITS")) > 0)
+      v.tc_min_units = atoi(env("FLEXQ_TC_MIN_UNITS"));
+    v.tc_align = !(env("FLEXQ_TC_ALIGN") && atoi(env("FLEXQ_TC_ALIGN")) == 0);
     return v;
   }();
   return t;
@@ -114,6 +117,28 @@ int device_sms() {
     sms[dev] = v > 0 ? v : 148;
   }
   return sms[dev];
+}
+
+int tc_grid(int64_t units, int64_t kbn, int min_pct) {
+  // Measured (tools/ab_tc_grid.sh): with every CTA inside one tile the split tiles have the
+  // fewest, equal contributors and the fixups shrink -- 7B q_proj M = 64 / 128 / 256 on
+  // kind::i8 21.5 / 30.4 / 32.1 -> 17.9 / 24.3 / 26.9 us, 13B gate_proj M = 128 on kind::f16
+  // 43.6 -> 27.9 us -- but a grid that leaves many SMs idle loses (7B down_proj at 64 of 148
+  // CTAs: 40.6 -> 48.4 us), hence the per-kernel floor.
+  const int64_t sms = device_sms();
+  int64_t c = units / tuning().tc_min_units;
+  if (c < 1) c = 1;
+  if (c > sms) c = sms;
+  if (tuning().tc_align && kbn > 0 && units % kbn == 0 && min_pct <= 100) {
+    const int64_t need = cdiv(units, c);
+    for (int64_t upc = need; upc <= kbn; upc++)
+      if (kbn % upc == 0) {
+        const int64_t ca = units / upc;
+        if (ca * 100 >= sms * min_pct) return (int)ca;
+        break;
+      }
+  }
+  return (int)c;
 }
 
 cudaError_t ensure_smem(const void* kern, int bytes) {
@@ -185,6 +210,8 @@ const char* flexq_tuning(void) {
     if (t.stream_max_m != d.stream_max_m) add("FLEXQ_STREAM_MAX_M", std::to_string(t.stream_max_m));
     if (t.stream_stages != d.stream_stages) add("FLEXQ_STREAM_STAGES", std::to_string(t.stream_stages));
     if (t.min_units != d.min_units) add("FLEXQ_MIN_UNITS", std::to_string(t.min_units));
+    if (t.tc_min_units != d.tc_min_units) add("FLEXQ_TC_MIN_UNITS", std::to_string(t.tc_min_units));
+    if (t.tc_align != d.tc_align) add("FLEXQ_TC_ALIGN", "0");
     desc = s.empty() ? "defaults" : s;
   });
   return desc.c_str();

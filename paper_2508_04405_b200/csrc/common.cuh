@@ -36,7 +36,13 @@ struct Tuning {
   int stream_max_m = 32;       // FLEXQ_STREAM_MAX_M: largest M on the streaming GEMV
   int stream_stages = -1;      // FLEXQ_STREAM_STAGES: 2/3/4 forced ring depth (-1: by size)
   int min_units = 4;           // FLEXQ_MIN_UNITS: units per warp with 4-stage rings
+  int tc_min_units = 1;        // FLEXQ_TC_MIN_UNITS: fewest stream-K units per tcgen05 CTA
+  bool tc_align = true;        // FLEXQ_TC_ALIGN=0: plain stream-K grids (A/B)
 };
+// CTAs of a persistent stream-K tcgen05 launch over `units` = tiles x kbn work items: one per
+// SM, or -- when that keeps at least min_pct % of the SMs busy -- the count that gives every
+// CTA a whole divisor of a tile's k-blocks (ranges aligned to tile fractions)
+int tc_grid(int64_t units, int64_t kbn, int min_pct);
 const Tuning& tuning();
 int device_sms();  // SM count of the current device (cached per device)
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, bytes)

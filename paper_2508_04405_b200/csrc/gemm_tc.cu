@@ -906,7 +906,6 @@ bool gemm_tc_supported(int64_t m, int64_t m_pad, int64_t spg) {
 
 static int tc_sms() { return device_sms(); }
 
-static int64_t tc_ctas(int64_t units) { return units < tc_sms() ? units : tc_sms(); }
 
 int64_t gemm_tc_workspace(int64_t m, int64_t n, int64_t k, int64_t gs) {
   T6Geom G(n, k, gs);
@@ -989,7 +988,7 @@ int gemm_tc_launch(const uint32_t* t6, const void* wscale, int scale_f16, const 
   p.tt = (int)cdiv(m, tn);
   const int64_t tiles = cdiv(n, kTcRows) * p.tt;
   p.units = tiles * G.kb;
-  p.nctas = (int)tc_ctas(p.units);
+  p.nctas = tc_grid(p.units, G.kb, 80);  // aligned only when >= 80 % of the SMs stay busy
   p.geo = G;
   p.partials = partials;
   p.y = y;
