@@ -358,10 +358,11 @@ int64_t flexq_act_m_pad(int64_t m) { return m < 1 ? 0 : tc_act_m_pad(m); }
 static std::atomic<int> g_tc16_mode{-1};  // flexq_set_tc16_route: -1 auto, 0 never, 1 always
 
 static bool tc16_route(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f16) {
-  if (m <= 32 || tuning().disable_tc16 || tuning().disable_tc || !gemm_tc16_supported(m, n, k, gs, scale_f16))
+  if (m <= 16 || tuning().disable_tc16 || tuning().disable_tc || !gemm_tc16_supported(m, n, k, gs, scale_f16))
     return false;
   const int mode = g_tc16_mode.load(std::memory_order_relaxed);
   if (mode >= 0) return mode == 1;
+  if (m <= 32) return false;  // 16 < M <= 32: the streaming GEMV or kind::i8 (measured faster)
   // Measured A/B against the INT8 kernel (tools/ab_tc16.sh, LLaMA-2 7B/13B/70B linears):
   // kind::f16 wins on layers of >= 8192 units (70B gate M = 64/128/256: 60/73/118 vs
   // 85/103/187 us) and loses on smaller ones (7B q_proj M = 128: 40 vs 31 us: too few k-blocks
@@ -390,7 +391,7 @@ static int64_t act_f16_offset(int64_t m, int64_t k, int64_t group_size) {
 
 int64_t flexq_act_buf_bytes(int64_t m, int64_t k, int64_t group_size) {
   const int64_t base = act_f16_offset(m, k, group_size);
-  if (m > 32 && group_size == 128 && k % 128 == 0)  // room for the fp16 operand (gemm_tc16)
+  if (m > 16 && group_size == 128 && k % 128 == 0)  // room for the fp16 operand (gemm_tc16)
     return base + flexq_act_m_pad(m) * k * 2;
   return base;
 }

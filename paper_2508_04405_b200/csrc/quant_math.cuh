@@ -22,6 +22,27 @@ __device__ __forceinline__ int quant_one(double v, double s, int bits) {
   return q < 0.0 ? -(int)a : (int)a;
 }
 
+// group_scale(peak, bits, fp16 = 1) in fp32: fp16(fl32(peak / lim)) equals fp16(fl64(peak /
+// lim)) for every positive fp16 peak and bits 2..8 (exhaustive, tools/check_f32_quant.c)
+__device__ __forceinline__ float group_scale_h(float peak, int bits, uint32_t* flag) {
+  const float lim = (float)((1 << (bits - 1)) - 1);
+  const float s = peak > 0.f ? __half2float(__float2half_rn(__fdiv_rn(peak, lim))) : 1.f;
+  if (!(s > 0.f) && flag) atomicOr(flag, FLEXQ_FLAG_NONPOS_SCALE);
+  return s;
+}
+
+// The same code when v and s are both fp16 values (fp16 input, fp16 scales), in fp32: one
+// correctly rounded fp32 quotient lies on the same side of every half-integer as the exact
+// quotient (or on it exactly), so roundf() of it equals floor(|fl64(v / s)| + 0.5) with its
+// sign -- checked exhaustively over all 2.0e9 (finite fp16 v, positive fp16 s) pairs
+// (tools/check_f32_quant.c).  ~8x fewer issue slots than the float64 divide.
+__device__ __forceinline__ int quant_one_h(float v, float s, int bits) {
+  const float lim = (float)((1 << (bits - 1)) - 1);
+  const float q = __fdiv_rn(v, s);
+  const float a = fminf(roundf(fabsf(q)), lim);
+  return q < 0.f ? -(int)a : (int)a;
+}
+
 // Non-finite inputs quantize to 0 (the caller raises the flag and zeroes the peak).
 __device__ __forceinline__ int code_of(double v, double s, int bits) {
   return isfinite(v) ? quant_one(v, s, bits) : 0;

@@ -281,17 +281,16 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
   // grid-stride over (row, group) items, two per pass with both loads issued first: the
   // grid is capped at one CTA per SM so that the quantizer's CTAs never take the register
   // room a persistent GEMM CTA launched behind it (PDL) needs on an SM
-  auto quantize_item = [&](int64_t item, uint2 raw) {
-    const int64_t r = item / ng, g = item - r * ng;
+  auto quantize_item = [&](int64_t r, int64_t g, uint2 raw) {
     const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
     const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-    const double v[4] = {(double)f01.x, (double)f01.y, (double)f23.x, (double)f23.y};
+    const float f[4] = {f01.x, f01.y, f23.x, f23.y};
     bool finite = true;
     float peak = 0.f;  // max of fp16 magnitudes: exact in fp32
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      finite &= isfinite(v[i]);
-      peak = fmaxf(peak, fabsf((float)v[i]));
+      finite &= isfinite(f[i]);
+      peak = fmaxf(peak, fabsf(f[i]));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
@@ -299,52 +298,85 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
       if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
       peak = 0.f;
     }
-    const double sc = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
-    int c[4], csum = 0;
+    int c[4];
+    double sc;
+    float sc32 = 0.f;
+    bool h = false;
+    if (A.fp16_scales) {
+      // fp16 scales (the production path): scale and codes in fp32, bit-identical to the
+      // float64 steps (group_scale_h, quant_one_h; exhaustive check tools/check_f32_quant.c)
+      sc32 = group_scale_h(peak, A.bits, lane == 0 ? A.flag : nullptr);
+      sc = (double)sc32;
+      h = sc32 > 0.f;
+    } else {
+      sc = group_scale((double)peak, A.bits, 0, lane == 0 ? A.flag : nullptr);
+    }
+    if (h) {
+      const float lim = (float)((1 << (A.bits - 1)) - 1);
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      c[i] = code_of(v[i], sc, A.bits);
-      csum += c[i];
+      for (int i = 0; i < 4; i++) {
+        const float q = __fdiv_rn(f[i], sc32);
+        const float a = fminf(roundf(fabsf(q)), lim);
+        const int ci = q < 0.f ? -(int)a : (int)a;
+        c[i] = isfinite(f[i]) ? ci : 0;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; i++) c[i] = code_of((double)f[i], sc, A.bits);
     }
     const uint32_t word = (uint32_t)(c[0] & 0xff) | ((uint32_t)(c[1] & 0xff) << 8) |
                           ((uint32_t)(c[2] & 0xff) << 16) | ((uint32_t)(c[3] & 0xff) << 24);
     if (A.codes) *reinterpret_cast<uint32_t*>(A.codes + r * A.cols + g * 128 + lane * 4) = word;
     if (A.act_frag)
       *reinterpret_cast<uint32_t*>(A.act_frag + operand_word_offset(g, r, A.m_pad, lane)) = word;
-    if (A.act_f16) {  // fp16(code * scale): the product is exact in double, one rounding
+    if (A.act_f16) {  // fp16(code * scale): the product is exact (fp32 for an fp16 scale), one rounding
       __half hv[4];
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int code = (int)(int8_t)((word >> (8 * i)) & 0xffu);
-        hv[i] = __double2half((double)code * sc);
-      }
+      for (int i = 0; i < 4; i++)
+        hv[i] = h ? __float2half_rn((float)c[i] * sc32) : __double2half((double)c[i] * sc);
       // columns 4L .. 4L+3 of the group: core L / 2 (8 k each), bytes 8 (L % 2) ..
       uint8_t* dst = reinterpret_cast<uint8_t*>(A.act_f16) +
                      ((g * (A.m_pad >> 3) + (r >> 3)) * 16 + (lane >> 1)) * 128 + (r & 7) * 16 + 8 * (lane & 1);
       *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(hv);
     }
+    if (A.act_corr) {
+      int csum = c[0] + c[1] + c[2] + c[3];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+      for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+      if (lane == 0) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
+    }
     if (lane == 0) {
       if (A.scales) A.scales[r * ng + g] = sc;
       if (A.act_scale) A.act_scale[g * A.m_pad + r] = (float)sc;
-      if (A.act_corr) A.act_corr[g * A.m_pad + r] = kCorrBias + 32 * csum;
       if (A.dbg) dbg_record(A.dbg, A.dbg_tag, dt0, dt1, dbg_now());
     }
   };
-  auto load = [&](int64_t item) {
-    const int64_t r = item / ng, g = item - r * ng;
+  auto load = [&](int64_t r, int64_t g) {
     return *reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(A.x) + r * A.cols +
                                            g * 128 + lane * 4);
   };
+  // (row, group) of items a and b = a + stride, advanced incrementally (no 64-bit division
+  // per item: it was a sizeable share of the kernel's instructions at large M)
   const int64_t stride = (int64_t)gridDim.x * 8;
-  for (int64_t a = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); a < items; a += 2 * stride) {
-    const int64_t b = a + stride;
-    const uint2 ra = load(a);
-    const uint2 rb = b < items ? load(b) : make_uint2(0u, 0u);
-    quantize_item(a, ra);
-    if (b < items) quantize_item(b, rb);
+  const int64_t a0 = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t sq = stride / ng, sr = stride - sq * ng;
+  int64_t ra = a0 / ng, ga = a0 - ra * ng;
+  int64_t rb = ra + sq, gb = ga + sr;
+  if (gb >= ng) { gb -= ng; rb++; }
+  auto advance = [&](int64_t& r, int64_t& g) {  // by 2 * stride
+    r += 2 * sq;
+    g += 2 * sr;
+    if (g >= ng) { g -= ng; r++; }
+    if (g >= ng) { g -= ng; r++; }
+  };
+  for (; ra < A.rows; advance(ra, ga), advance(rb, gb)) {
+    const uint2 xa = load(ra, ga);
+    const bool hb = rb < A.rows;
+    const uint2 xb = hb ? load(rb, gb) : make_uint2(0u, 0u);
+    quantize_item(ra, ga, xa);
+    if (hb) quantize_item(rb, gb, xb);
   }
+  (void)items;
 }
 
 constexpr int64_t kWarpGroupMax = 1024;
@@ -357,7 +389,10 @@ static void launch_quantize(const QuantArgs& A, cudaStream_t st) {
     const int sms = device_sms();
     // decode batches feed the persistent GEMV (3 CTAs per SM, registers nearly full): at most
     // one quantizer CTA per SM.  Larger batches keep one warp per item (one wave).
-    const int64_t ctas = (A.rows <= 16 && cdiv(items, 8) > sms) ? sms : cdiv(items, 8);
+    // Larger batches: one wave of 8 CTAs per SM, every warp grid-striding over its items with
+    // two loads in flight (one warp per item took 6+ waves: 70B down_proj M = 256, 57344 items)
+    const int64_t ctas = (A.rows <= 16 && cdiv(items, 8) > sms) ? sms
+                         : cdiv(items, 8) > 8 * (int64_t)sms ? 8 * (int64_t)sms : cdiv(items, 8);
     launch_pdl(quantize_g128_kernel, dim3((unsigned)ctas), dim3(256), 0, st, A);
     return;
   }
