@@ -200,14 +200,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_block_kernel(
     for (int i = 0; i < 4; i++) op[i] = oh[i];
   }
   // o_proj activation quantizer for (token b, group hh): lane holds columns 4*lane..+3
-  double v[4];
+  float v[4];
   bool finite = true;
   float peak = 0.f;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    v[i] = (double)__half2float(oh[i]);
+    v[i] = __half2float(oh[i]);
     finite &= isfinite(v[i]);
-    peak = fmaxf(peak, fabsf(__half2float(oh[i])));
+    peak = fmaxf(peak, fabsf(v[i]));
   }
 #pragma unroll
   for (int s = 16; s; s >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, s));
@@ -215,14 +215,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32) attn_block_kernel(
     if (lane == 0) atomicOr(flag, FLEXQ_FLAG_NONFINITE);
     peak = 0.f;
   }
-  const double sc = group_scale((double)peak, bits, 1, lane == 0 ? flag : nullptr);
+  int cd[4];
+  const double sc = codes4_fp16(v, peak, bits, 1, lane == 0 ? flag : nullptr, cd);
   int csum = 0;
   uint32_t word = 0;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    const int code = isfinite(v[i]) ? quant_one(v[i], sc, bits) : 0;
-    csum += code;
-    word |= (uint32_t)(code & 0xff) << (8 * i);
+    csum += cd[i];
+    word |= (uint32_t)(cd[i] & 0xff) << (8 * i);
   }
   *reinterpret_cast<uint32_t*>(act_frag + operand_word_offset(hh, b, m_pad, lane)) = word;
 #pragma unroll

@@ -48,6 +48,28 @@ __device__ __forceinline__ int code_of(double v, double s, int bits) {
   return isfinite(v) ? quant_one(v, s, bits) : 0;
 }
 
+// Codes of four fp16-valued inputs of one group and the group's scale (peak = the group's
+// max |v|, 0 when the group holds a non-finite value): fp32 steps for fp16 scales, float64
+// otherwise -- the same results either way.
+__device__ __forceinline__ double codes4_fp16(const float f[4], float peak, int bits, int fp16,
+                                              uint32_t* flag, int c[4]) {
+  if (fp16) {
+    const float s = group_scale_h(peak, bits, flag);
+    if (s > 0.f) {
+#pragma unroll
+      for (int i = 0; i < 4; i++) c[i] = isfinite(f[i]) ? quant_one_h(f[i], s, bits) : 0;
+      return (double)s;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) c[i] = code_of((double)f[i], (double)s, bits);
+    return (double)s;
+  }
+  const double s = group_scale((double)peak, bits, 0, flag);
+#pragma unroll
+  for (int i = 0; i < 4; i++) c[i] = code_of((double)f[i], s, bits);
+  return s;
+}
+
 // Byte offset of the 4 consecutive operand bytes holding columns 4*lane .. 4*lane+3 of
 // group g (group = one 128-slot k-block) for token r.
 __device__ __forceinline__ int64_t operand_word_offset(int64_t g, int64_t r, int64_t m_pad, int lane) {

@@ -545,16 +545,16 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_quant_kernel(FusedQuan
   if (A.gs == 128 && (K & 127) == 0) {
     // lane L: the 4 consecutive columns 4L..4L+3 -> 4 consecutive operand bytes, one store
     const int64_t c0 = g * 128 + lane * 4;
-    double v[4];
+    float v[4];
     bool finite = true;
     float peak = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       const __half hv = fused_h(F, xr, c0 + i, inv);
       if (F.h_out) F.h_out[r * K + c0 + i] = hv;
-      v[i] = (double)__half2float(hv);
+      v[i] = __half2float(hv);
       finite &= isfinite(v[i]);
-      peak = fmaxf(peak, fabsf(__half2float(hv)));
+      peak = fmaxf(peak, fabsf(v[i]));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
@@ -562,14 +562,14 @@ __global__ void __launch_bounds__(kFusedWarps * 32) fused_quant_kernel(FusedQuan
       if (lane == 0) atomicOr(A.flag, FLEXQ_FLAG_NONFINITE);
       peak = 0.f;
     }
-    const double s = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
+    int cd[4];
+    const double s = codes4_fp16(v, peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr, cd);
     int csum = 0;
     uint32_t word = 0;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      const int code = isfinite(v[i]) ? quant_one(v[i], s, A.bits) : 0;
-      csum += code;
-      word |= (uint32_t)(code & 0xff) << (8 * i);
+      csum += cd[i];
+      word |= (uint32_t)(cd[i] & 0xff) << (8 * i);
     }
     const int jj = lane >> 3, hh = (lane >> 2) & 1, t = lane & 3;
     const int64_t off = ((g * (A.m_pad >> 3) + (r >> 3)) * 8 + 2 * t + hh) * 128 + (r & 7) * 16 + jj * 4;
