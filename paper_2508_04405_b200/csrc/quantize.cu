@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
       sc = (double)sc32;
       h = sc32 > 0.f;
     } else {
-      sc = group_scale((double)peak, A.bits, 0, lane == 0 ? A.flag : nullptr);
+      sc = group_scale((double)peak, A.bits, A.fp16_scales, lane == 0 ? A.flag : nullptr);
     }
     if (h) {
       const float lim = (float)((1 << (A.bits - 1)) - 1);
@@ -355,28 +355,17 @@ __global__ void __launch_bounds__(256) quantize_g128_kernel(QuantArgs A) {
     return *reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(A.x) + r * A.cols +
                                            g * 128 + lane * 4);
   };
-  // (row, group) of items a and b = a + stride, advanced incrementally (no 64-bit division
-  // per item: it was a sizeable share of the kernel's instructions at large M)
   const int64_t stride = (int64_t)gridDim.x * 8;
-  const int64_t a0 = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int64_t sq = stride / ng, sr = stride - sq * ng;
-  int64_t ra = a0 / ng, ga = a0 - ra * ng;
-  int64_t rb = ra + sq, gb = ga + sr;
-  if (gb >= ng) { gb -= ng; rb++; }
-  auto advance = [&](int64_t& r, int64_t& g) {  // by 2 * stride
-    r += 2 * sq;
-    g += 2 * sr;
-    if (g >= ng) { g -= ng; r++; }
-    if (g >= ng) { g -= ng; r++; }
-  };
-  for (; ra < A.rows; advance(ra, ga), advance(rb, gb)) {
+  for (int64_t a = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); a < items; a += 2 * stride) {
+    const int64_t b = a + stride;
+    const int64_t ra = a / ng, ga = a - ra * ng;
     const uint2 xa = load(ra, ga);
-    const bool hb = rb < A.rows;
+    const bool hb = b < items;
+    const int64_t rb = hb ? b / ng : 0, gb = b - rb * ng;
     const uint2 xb = hb ? load(rb, gb) : make_uint2(0u, 0u);
     quantize_item(ra, ga, xa);
     if (hb) quantize_item(rb, gb, xb);
   }
-  (void)items;
 }
 
 constexpr int64_t kWarpGroupMax = 1024;
