@@ -551,8 +551,9 @@ int gemm_tc16_launch(const uint32_t* t6, const void* wscale, const void* act_f16
   p.kbn = (int)G.kb;
   p.rg = (int)G.rg;
   p.units = cdiv(n, 128) * G.kb;
-  // aligned grids from TN = 128 up (at TN = 64 they measured slower on 70B down_proj)
-  p.nctas = tc_grid(p.units, G.kb, tn >= 128 ? 50 : 101);
+  // aligned grids from TN = 128 up; at TN = 64 only on layers of <= 8192 units with >= 70 % of
+  // the SMs busy (13B gate_proj M = 64: 31.9 -> 24.8 us; 70B down_proj, 14336 units, slower)
+  p.nctas = tc_grid(p.units, G.kb, tn >= 128 ? 50 : p.units <= 8192 ? 70 : 101);
   const int64_t sms = device_sms();
   p.y = y;
   p.out_dtype = out_dtype;
