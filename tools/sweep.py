@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--ms", default="1,2,4,8,16,32,64,128,256")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--no-mma", action="store_true")
+    ap.add_argument("--tc16-route", type=int, default=-1, choices=[-1, 0, 1],
+                    help="flexq_set_tc16_route for the run: -1 auto, 0 never, 1 always (M > 16)")
     ap.add_argument("--no-cublas", action="store_true",
                     help="skip the cuBLAS fp16 (W16A16) and cuBLASLt int8 (W8A8) comparators")
     args = ap.parse_args()
@@ -56,6 +58,8 @@ def main():
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     dev = torch.device("cuda", 0)
     L = _lib.lib()
+    if args.tc16_route != -1:
+        L.flexq_set_tc16_route(args.tc16_route)
     shapes = MODELS[args.model]
     if args.model != "llama2-70b":
         shapes = unfused(shapes)
