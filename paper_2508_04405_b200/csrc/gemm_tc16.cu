@@ -235,6 +235,13 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
   const int64_t cta = blockIdx.x, P = p.nctas, U = p.units;
   const int64_t u0 = t16_start(cta, U, P), u1 = t16_start(cta + 1, U, P);
   const int kbn = p.kbn;
+  // debug builds: per-CTA globaltimer marks {entry, MMA loop start, MMA loop end, exit}
+  auto cta_mark = [&](int i) {
+    if constexpr (FLEXQ_TC16_TIMELINE) {
+      if (p.tl) p.tl[32 + 1024 + blockIdx.x * 4 + i] = dbg_now();
+    }
+  };
+  if (threadIdx.x == 0) cta_mark(0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::SW; i++) { mbar_init(&wfull[i], 2); mbar_init(&wempty[i], kT16ConvWarps); }
@@ -359,6 +366,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
     int64_t kb = u0 % kbn;
     T16Prof pf;
     pf.start();
+    if (lane == 0) cta_mark(1);
     for (int64_t u = u0; u < u1; u++) {
       const bool tile_end = kb == kbn - 1 || u == u1 - 1;
       if (++kb == kbn) kb = 0;
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
       }
       if (++ai == C::SA) { ai = 0; aph ^= 1u; }
     }
-    if (lane == 0) pf.flush(p, 3, u1 - u0);
+    if (lane == 0) { pf.flush(p, 3, u1 - u0); cta_mark(2); }
     if constexpr (FLEXQ_TC16_TIMELINE) {  // every CTA: its MMA loop's total cycles
       if (lane == 0 && p.tl) p.tl[32 + blockIdx.x] = pf.acc[0] + pf.acc[1] + pf.acc[2];
     }
@@ -488,6 +496,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
 
   tc16::fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) cta_mark(3);
   if (warp == kT16WarpMma) {
     tc16::fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols) : "memory");
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(kT16Threads, 1) gemm_tc16_kernel(T16Params p) 
 // ---- host side ------------------------------------------------------------------------------
 static long long* g_t16_tl = nullptr;
 extern "C" int flexq_debug_tc16_timeline(long long* host, int max_entries) {
-  const int n = 32 + 1024;
+  const int n = 32 + 1024 + 4 * 1024;
   if (!g_t16_tl || max_entries < n) return 0;
   cudaDeviceSynchronize();
   cudaMemcpy(host, g_t16_tl, n * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -563,8 +572,8 @@ int gemm_tc16_launch(const uint32_t* t6, const void* wscale, const void* act_f16
   p.counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) +
                                            cdiv(s2 * 2 * tn * 128 * 4, 256) * 256);
   if (tuning().tc_timeline) {
-    if (!g_t16_tl) cudaMalloc(&g_t16_tl, (32 + 1024) * sizeof(long long));
-    cudaMemsetAsync(g_t16_tl, 0, (32 + 1024) * sizeof(long long), st);
+    if (!g_t16_tl) cudaMalloc(&g_t16_tl, (32 + 1024 + 4 * 1024) * sizeof(long long));
+    cudaMemsetAsync(g_t16_tl, 0, (32 + 1024 + 4 * 1024) * sizeof(long long), st);
     p.tl = g_t16_tl;
   }
   const bool f32 = out_dtype == FLEXQ_OUT_F32;

@@ -27,8 +27,8 @@ def main():
     L = _lib.lib()
     fn = L.flexq_debug_tc16_timeline
     fn.restype = ctypes.c_int
-    buf = (ctypes.c_longlong * (32 + 1024))()
-    if fn(buf, 32 + 1024) == 0:
+    buf = (ctypes.c_longlong * (32 + 1024 + 4 * 1024))()
+    if fn(buf, 32 + 1024 + 4 * 1024) == 0:
         print("no profile: build with -DFLEXQ_TC16_TIMELINE=1 (tools/build_debug.sh) and set FLEXQ_LIB")
         return
     allv = np.frombuffer(buf, dtype=np.int64)
@@ -38,6 +38,16 @@ def main():
     if len(per):
         print(f"MMA loop cycles over {len(per)} CTAs: min {per.min()} median {int(np.median(per))} "
               f"max {per.max()} (CTA 0: {per[0]})")
+    marks = allv[32 + 1024:].reshape(1024, 4)
+    marks = marks[marks[:, 0] > 0]
+    if len(marks):
+        t0 = marks[:, 0].min()
+        q = lambda a: f"min {a.min() / 1e3:6.2f} med {np.median(a) / 1e3:6.2f} max {a.max() / 1e3:6.2f} us"
+        print(f"{len(marks)} CTAs (globaltimer): entry after first entry {q(marks[:, 0] - t0)}")
+        print(f"  entry -> MMA loop start {q(marks[:, 1] - marks[:, 0])}")
+        print(f"  MMA loop                {q(marks[:, 2] - marks[:, 1])}")
+        print(f"  loop end -> CTA exit    {q(marks[:, 3] - marks[:, 2])}")
+        print(f"  last exit after first entry {(marks[:, 3].max() - t0) / 1e3:.2f} us")
     roles = [("converter w0", ["wait raw", "wait A/B stage", "convert", "store+arrive"]),
              ("weight producer", ["wait free raw", "issue"]),
              ("B producer", ["wait free stage", "issue"]),
