@@ -363,14 +363,16 @@ static bool tc16_route(int64_t m, int64_t n, int64_t k, int64_t gs, int scale_f1
   const int mode = g_tc16_mode.load(std::memory_order_relaxed);
   if (mode >= 0) return mode == 1;
   if (m <= 32) return false;  // 16 < M <= 32: the streaming GEMV or kind::i8 (measured faster)
-  // Measured A/B against the INT8 kernel (tools/ab_tc16.sh, LLaMA-2 7B/13B/70B linears):
-  // kind::f16 wins on layers of >= 8192 units (70B gate M = 64/128/256: 60/73/118 vs
-  // 85/103/187 us) and loses on smaller ones (7B q_proj M = 128: 40 vs 31 us: too few k-blocks
-  // per CTA to fill its deeper pipeline).  For 128 < M <= 256 (one 256-token tile) it also
-  // needs a wide or long layer (13B down_proj 5120 x 13824 M = 256: 82 vs 68 us).
+  // Measured A/B against the INT8 kernel (tools/ab_tc16.sh, sweep --tc16-route, LLaMA-2
+  // 7B/13B/70B linears, aligned grids): kind::f16 wins on layers of >= 8192 units (70B gate
+  // M = 64/128/256: 60/74/120 vs 85/103/187 us) and loses on smaller ones at M <= 128 (7B
+  // q_proj M = 128: 40 vs 31 us: too few k-blocks per CTA to fill its deeper pipeline).  For
+  // 128 < M <= 256 (one 256-token tile) it also wins on wide layers (7B gate_proj 11008 x 4096
+  // M = 256: 36.8 vs 52.3 us; 70B o_proj 54.5 vs 60.0 us) but not on narrow ones (7B down_proj
+  // 4096 x 11008: 68.1 vs 49.5 us).
   const int64_t units = cdiv(n, 64) * cdiv(k, 128);
-  if (units < 8192) return false;
-  return m <= 128 || n >= 10240 || units >= 16384;
+  if (m <= 128) return units >= 8192;
+  return units >= 8192 || n >= 8192;
 }
 
 int flexq_set_tc16_route(int mode) {

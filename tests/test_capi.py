@@ -80,8 +80,8 @@ def test_product_path_has_no_cpu_fallback():
 
 
 def test_tc16_route_rule_and_override():
-    """The kind::f16 batched route: measured size rule by default (>= 8192 units; 128 < M <=
-    256 only on wide or long layers), a process-wide override for A/B runs and tests."""
+    """The kind::f16 batched route: measured size rule by default (>= 8192 units; for 128 < M
+    <= 256 also any layer of >= 8192 rows), a process-wide override for A/B runs and tests."""
     L = _lib.load()  # host-only: routing needs no device
     assert L.flexq_set_tc16_route(5) == -2  # invalid mode: rejected, state unchanged
     prev = L.flexq_set_tc16_route(-1)
@@ -89,6 +89,9 @@ def test_tc16_route_rule_and_override():
         assert L.flexq_linear_kernel(64, 28672, 8192, 128, 1) == _lib.KERNEL_TC16   # 70B gate
         assert L.flexq_linear_kernel(256, 28672, 8192, 128, 1) == _lib.KERNEL_TC16  # wide
         assert L.flexq_linear_kernel(256, 8192, 28672, 128, 1) == _lib.KERNEL_TC16  # long
+        assert L.flexq_linear_kernel(256, 11008, 4096, 128, 1) == _lib.KERNEL_TC16  # wide, M > 128
+        assert L.flexq_linear_kernel(128, 11008, 4096, 128, 1) != _lib.KERNEL_TC16  # same, M <= 128
+        assert L.flexq_linear_kernel(256, 4096, 11008, 128, 1) != _lib.KERNEL_TC16  # narrow
         assert L.flexq_linear_kernel(64, 4096, 4096, 128, 0) != _lib.KERNEL_TC16    # fp32 scales
         assert L.flexq_set_tc16_route(1) == -1
         assert L.flexq_linear_kernel(64, 4096, 4096, 128, 1) == _lib.KERNEL_TC16    # forced
